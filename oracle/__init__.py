@@ -1,0 +1,182 @@
+"""Double-precision CPU oracle for the NURBS-Diff hot path (ctypes over nurbs_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package. The product package
+``paper_2104_14547_b200`` never imports it and shares no code with it.
+
+Every function follows a cited passage of /root/reference/PAPER.md (see nurbs_oracle.c);
+inputs are fp32 arrays cast exactly to fp64 (R19 of DESIGN.md §3), outputs are fp64.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "nurbs_oracle.c")
+_LIB = os.path.join(_HERE, "libnurbs_oracle.so")
+
+REF_OK, REF_E_ARG, REF_E_KNOTS, REF_E_DOMAIN, REF_E_WEIGHT = 0, 1, 3, 4, 5
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain -O2, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        d, i32 = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)
+        c_int = ctypes.c_int
+        L.nurbs_ref_find_span.argtypes = [c_int, c_int, d, ctypes.c_double]
+        L.nurbs_ref_find_span.restype = c_int
+        L.nurbs_ref_basis_funs.argtypes = [c_int, ctypes.c_double, c_int, d, d]
+        L.nurbs_ref_basis_funs.restype = None
+        L.nurbs_ref_basis_dense.argtypes = [c_int, c_int, d, ctypes.c_double, d]
+        L.nurbs_ref_basis_dense.restype = None
+        L.nurbs_ref_check_knots.argtypes = [c_int, c_int, d]
+        L.nurbs_ref_spans.argtypes = [c_int, c_int, d, c_int, d, i32, d]
+        surf = [c_int] * 8 + [d, d, d, d, d]
+        L.nurbs_ref_surface_fwd.argtypes = surf + [d]
+        L.nurbs_ref_surface_bwd.argtypes = surf + [d, d]
+        L.nurbs_ref_surface_bwd_eq89.argtypes = surf + [d, d]
+        L.nurbs_ref_surface_bwd_selected.argtypes = surf + [d, c_int, i32, i32, i32, d]
+        L.nurbs_ref_surface_dense.argtypes = [c_int] * 6 + [d, d, d, d, d, d, d]
+        L.nurbs_ref_curve_fwd.argtypes = [c_int] * 5 + [d, d, d, d]
+        L.nurbs_ref_curve_bwd.argtypes = [c_int] * 5 + [d, d, d, d, d]
+        _lib = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _d(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _pi(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _chk(st: int, what: str):
+    if st != REF_OK:
+        raise OracleError(f"{what}: oracle status {st}")
+
+
+def find_span(n: int, p: int, U, u: float) -> int:
+    U = _d(U)
+    return int(lib().nurbs_ref_find_span(n, p, _p(U), float(u)))
+
+
+def basis_funs(s: int, u: float, p: int, U) -> np.ndarray:
+    U = _d(U)
+    N = np.zeros(p + 1)
+    lib().nurbs_ref_basis_funs(s, float(u), p, _p(U), _p(N))
+    return N
+
+
+def basis_dense(n: int, p: int, U, u: float) -> np.ndarray:
+    U = _d(U)
+    N = np.zeros(n)
+    lib().nurbs_ref_basis_dense(n, p, _p(U), float(u), _p(N))
+    return N
+
+
+def spans(n: int, p: int, U, s) -> tuple[np.ndarray, np.ndarray]:
+    U, s = _d(U), _d(s)
+    sp = np.zeros(len(s), dtype=np.int32)
+    N = np.zeros((len(s), p + 1))
+    _chk(lib().nurbs_ref_spans(n, p, _p(U), len(s), _p(s), _pi(sp), _p(N)), "spans")
+    return sp, N
+
+
+def _surf_args(ctrl, U, V, u, v, p, q, knots_batched):
+    ctrl = _d(ctrl)
+    B, n, m, four = ctrl.shape
+    assert four == 4
+    U, V, u, v = _d(U), _d(V), _d(u), _d(v)
+    return ctrl, U, V, u, v, (B, n, m, p, q, len(u), len(v), int(knots_batched))
+
+
+def surface_fwd(ctrl, U, V, u, v, p: int, q: int, knots_batched: bool = False) -> np.ndarray:
+    ctrl, U, V, u, v, dims = _surf_args(ctrl, U, V, u, v, p, q, knots_batched)
+    B, n, m, _, _, n_u, n_v, _ = dims
+    out = np.zeros((B, n_u, n_v, 3))
+    _chk(lib().nurbs_ref_surface_fwd(*dims, _p(ctrl), _p(U), _p(V), _p(u), _p(v), _p(out)), "surface_fwd")
+    return out
+
+
+def surface_bwd(ctrl, U, V, u, v, gout, p: int, q: int, knots_batched: bool = False,
+                form: str = "H") -> np.ndarray:
+    """Gradient [B][n][m][4] = dL/d(x,y,z,w). form='H' homogeneous, 'E' literal Eq.8/9."""
+    ctrl, U, V, u, v, dims = _surf_args(ctrl, U, V, u, v, p, q, knots_batched)
+    B, n, m = dims[:3]
+    g = _d(gout)
+    assert g.shape == (B, dims[5], dims[6], 3)
+    grad = np.zeros((B, n, m, 4))
+    fn = lib().nurbs_ref_surface_bwd if form == "H" else lib().nurbs_ref_surface_bwd_eq89
+    _chk(fn(*dims, _p(ctrl), _p(U), _p(V), _p(u), _p(v), _p(g), _p(grad)), "surface_bwd")
+    return grad
+
+
+def surface_bwd_selected(ctrl, U, V, u, v, gout, p, q, sel, knots_batched=False) -> np.ndarray:
+    """Eq.8/9 gradient at selected control points sel = [(k, i, j), ...] -> [len(sel)][4]."""
+    ctrl, U, V, u, v, dims = _surf_args(ctrl, U, V, u, v, p, q, knots_batched)
+    g = _d(gout)
+    sel = np.asarray(sel, dtype=np.int32).reshape(-1, 3)
+    order = np.lexsort((sel[:, 2], sel[:, 1], sel[:, 0]))  # group by surface (spans cached per k)
+    ss = np.ascontiguousarray(sel[order])
+    k, i, j = (np.ascontiguousarray(ss[:, c]) for c in range(3))
+    out = np.zeros((len(ss), 4))
+    _chk(lib().nurbs_ref_surface_bwd_selected(*dims, _p(ctrl), _p(U), _p(V), _p(u), _p(v), _p(g),
+                                              len(ss), _pi(k), _pi(i), _pi(j), _p(out)), "bwd_selected")
+    res = np.zeros_like(out)
+    res[order] = out
+    return res
+
+
+def surface_dense(ctrl2d, U, V, u, v, p, q, jacobian: bool = False):
+    """Brute force on one surface: (out [n_u][n_v][3], J or None)."""
+    ctrl = _d(ctrl2d)
+    n, m, _ = ctrl.shape
+    U, V, u, v = _d(U), _d(V), _d(u), _d(v)
+    out = np.zeros((len(u), len(v), 3))
+    J = np.zeros((len(u) * len(v) * 3, n * m * 4)) if jacobian else None
+    _chk(lib().nurbs_ref_surface_dense(n, m, p, q, len(u), len(v), _p(ctrl), _p(U), _p(V), _p(u), _p(v),
+                                       _p(out), _p(J) if jacobian else None), "surface_dense")
+    return out, J
+
+
+def curve_fwd(ctrl, U, u, p: int, knots_batched: bool = False) -> np.ndarray:
+    ctrl, U, u = _d(ctrl), _d(U), _d(u)
+    B, n, _ = ctrl.shape
+    out = np.zeros((B, len(u), 3))
+    _chk(lib().nurbs_ref_curve_fwd(B, n, p, len(u), int(knots_batched), _p(ctrl), _p(U), _p(u), _p(out)),
+         "curve_fwd")
+    return out
+
+
+def curve_bwd(ctrl, U, u, gout, p: int, knots_batched: bool = False) -> np.ndarray:
+    ctrl, U, u, g = _d(ctrl), _d(U), _d(u), _d(gout)
+    B, n, _ = ctrl.shape
+    grad = np.zeros((B, n, 4))
+    _chk(lib().nurbs_ref_curve_bwd(B, n, p, len(u), int(knots_batched), _p(ctrl), _p(U), _p(u), _p(g),
+                                   _p(grad)), "curve_bwd")
+    return grad

@@ -1,0 +1,154 @@
+"""Seeded synthetic inputs for the NURBS-Diff hot path (DESIGN.md §4 "input recipe").
+
+This module holds no arithmetic of the method: it only builds knot vectors, parameter grids,
+control nets, weights and upstream gradients as fp32 numpy arrays. The SAME arrays feed the
+CUDA path and the oracle. Generator: numpy PCG64, seed = config number unless given.
+
+Shapes follow BASELINE.json `configs` and SURVEY.md §8(d):
+  cfg1  cubic curve, 6 ctrl, clamped uniform knots, 100 samples
+  cfg2  bicubic 8x8 net, random weights, 64x64 grid
+  cfg3  bicubic 32x32 net, 512x512 grid (fitting workload)
+  cfg4  4096 bicubic 16x16 nets, 128x128 grid (decoder batch)
+  cfg5  one bicubic 256x256 net, 8192x8192 grid
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+f32 = np.float32
+
+
+def clamped_uniform_knots(n: int, p: int) -> np.ndarray:
+    """Clamped uniform knot vector (reading R7): p+1 zeros, fp32(k)/fp32(n-p) for k=1..n-p-1,
+    p+1 ones. Length n+p+1."""
+    inner = [f32(k) / f32(n - p) for k in range(1, n - p)]
+    return np.array([0.0] * (p + 1) + inner + [1.0] * (p + 1), dtype=f32)
+
+
+def random_clamped_knots(rng: np.random.Generator, n: int, p: int, min_gap: float = 0.0) -> np.ndarray:
+    """Clamped knots with sorted random interior knots (per-surface knots, Alg.1 U_k)."""
+    inner = np.sort(rng.uniform(0.02, 0.98, size=n - p - 1).astype(f32))
+    return np.concatenate([np.zeros(p + 1, f32), inner, np.ones(p + 1, f32)]).astype(f32)
+
+
+def uniform_grid(n_s: int) -> np.ndarray:
+    """Inclusive uniform samples of [0,1] (reading R8): fp32(a)/fp32(n_s-1); n_s==1 -> [0]."""
+    if n_s == 1:
+        return np.zeros(1, dtype=f32)
+    return (np.arange(n_s, dtype=f32) / f32(n_s - 1)).astype(f32)
+
+
+def lattice_net(rng: np.random.Generator, B: int, n: int, m: int, sigma: float = 0.1,
+                wlo: float = 0.5, whi: float = 1.5) -> np.ndarray:
+    """ctrl[B][n][m][4] = (i/(n-1), j/(m-1), 0) + N(0, sigma)^3, w ~ U(wlo, whi) (R15)."""
+    ii, jj = np.meshgrid(np.arange(n, dtype=f32) / f32(max(n - 1, 1)),
+                         np.arange(m, dtype=f32) / f32(max(m - 1, 1)), indexing="ij")
+    ctrl = np.empty((B, n, m, 4), dtype=f32)
+    ctrl[..., 0] = ii
+    ctrl[..., 1] = jj
+    ctrl[..., 2] = 0.0
+    ctrl[..., :3] += rng.normal(0.0, sigma, size=(B, n, m, 3)).astype(f32)
+    ctrl[..., 3] = rng.uniform(wlo, whi, size=(B, n, m)).astype(f32)
+    return ctrl
+
+
+def random_net(rng: np.random.Generator, shape, wlo: float = 0.5, whi: float = 1.5) -> np.ndarray:
+    ctrl = np.empty(tuple(shape) + (4,), dtype=f32)
+    ctrl[..., :3] = rng.uniform(-1.0, 1.0, size=tuple(shape) + (3,)).astype(f32)
+    ctrl[..., 3] = rng.uniform(wlo, whi, size=tuple(shape)).astype(f32)
+    return ctrl
+
+
+def normal(rng: np.random.Generator, shape) -> np.ndarray:
+    return rng.standard_normal(size=shape, dtype=f32)
+
+
+@dataclass
+class Surfaces:
+    """One synthetic surface workload (all fp32, C-contiguous)."""
+    name: str
+    p: int
+    q: int
+    ctrl: np.ndarray          # [B][n][m][4]
+    U: np.ndarray             # [n+p+1] or [B][n+p+1]
+    V: np.ndarray
+    u: np.ndarray             # [n_u]
+    v: np.ndarray             # [n_v]
+    knots_batched: bool = False
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def B(self): return self.ctrl.shape[0]
+    @property
+    def n(self): return self.ctrl.shape[1]
+    @property
+    def m(self): return self.ctrl.shape[2]
+    @property
+    def n_u(self): return len(self.u)
+    @property
+    def n_v(self): return len(self.v)
+    @property
+    def points(self): return self.B * self.n_u * self.n_v
+
+    def grad_out(self, seed: int | None = None) -> np.ndarray:
+        rng = np.random.default_rng(seed if seed is not None else 1000 + sum(self.name.encode()))
+        return normal(rng, (self.B, self.n_u, self.n_v, 3))
+
+
+@dataclass
+class Curves:
+    name: str
+    p: int
+    ctrl: np.ndarray          # [B][n][4]
+    U: np.ndarray
+    u: np.ndarray
+    knots_batched: bool = False
+
+    @property
+    def B(self): return self.ctrl.shape[0]
+    @property
+    def n(self): return self.ctrl.shape[1]
+    @property
+    def n_u(self): return len(self.u)
+
+    def grad_out(self, seed: int = 11) -> np.ndarray:
+        return normal(np.random.default_rng(seed), (self.B, self.n_u, 3))
+
+
+def config1(seed: int = 1) -> Curves:
+    rng = np.random.default_rng(seed)
+    n, p = 6, 3
+    return Curves("cfg1", p, random_net(rng, (1, n)), clamped_uniform_knots(n, p), uniform_grid(100))
+
+
+def surfaces(name: str, B: int, n: int, m: int, p: int, q: int, n_u: int, n_v: int, seed: int,
+             knots_batched: bool = False, sigma: float = 0.1) -> Surfaces:
+    rng = np.random.default_rng(seed)
+    ctrl = lattice_net(rng, B, n, m, sigma)
+    if knots_batched:
+        U = np.stack([random_clamped_knots(rng, n, p) for _ in range(B)])
+        V = np.stack([random_clamped_knots(rng, m, q) for _ in range(B)])
+    else:
+        U, V = clamped_uniform_knots(n, p), clamped_uniform_knots(m, q)
+    return Surfaces(name, p, q, ctrl, U, V, uniform_grid(n_u), uniform_grid(n_v), knots_batched)
+
+
+def config2(seed: int = 2) -> Surfaces:
+    return surfaces("cfg2", 1, 8, 8, 3, 3, 64, 64, seed)
+
+
+def config3(seed: int = 3) -> Surfaces:
+    return surfaces("cfg3", 1, 32, 32, 3, 3, 512, 512, seed)
+
+
+def config4(seed: int = 4, B: int = 4096, knots_batched: bool = False) -> Surfaces:
+    return surfaces("cfg4", B, 16, 16, 3, 3, 128, 128, seed, knots_batched)
+
+
+def config5(seed: int = 5, n_u: int = 8192, n_v: int = 8192) -> Surfaces:
+    return surfaces("cfg5", 1, 256, 256, 3, 3, n_u, n_v, seed)
+
+
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
