@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the NURBS-Diff hot path on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4|5] [--impl reference]
+
+A step is one pass of the whole hot path over one batch: nurbs_surface_fwd (FindSpan, basis,
+homogeneous banded sum, rational divide) then nurbs_surface_bwd (dL/dP, dL/dw, zero knot
+gradients), through the C ABI, on BASELINE.json's config 4 (4096 bicubic 16x16 NURBS
+surfaces, 128x128 grid per surface) — per rank, weak scaling (batch sharding, no
+collective). --config 5 runs the single 256x256 surface on the 8192^2 grid with its u-rows
+sharded over the ranks and one NCCL all-reduce of the gradients (strong scaling).
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §6 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "NURBS surface points/sec fwd and fwd+bwd (fp32); achieved HBM GB/s vs peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=4, choices=[4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="oracle cpu_baseline time budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(kernel: str, config: int):
+    """dram__bytes_read+write per launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d[f"cfg{config}"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML samples of SM clock + clock-event reasons during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- oracle legs
+def oracle_rate(seconds: float, config: int):
+    """The fp64 CPU oracle (oracle/, as it stands, single-threaded) on a bounded sample of
+    the same workload. Returns (points/s, sample description, cores)."""
+    import numpy as np
+
+    import oracle
+    import workloads as wl
+    oracle.build()
+    rng = np.random.default_rng(99)
+    pts, t_used, batches = 0, 0.0, 0
+    if config == 4:
+        w = wl.config4(B=64)
+        g = rng.standard_normal((64, 128, 128, 3), dtype=np.float32)
+        while t_used < seconds and batches < 64:
+            t0 = time.perf_counter()
+            oracle.surface_fwd(w.ctrl, w.U, w.V, w.u, w.v, w.p, w.q)
+            oracle.surface_bwd(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q)
+            t_used += time.perf_counter() - t0
+            pts += w.points
+            batches += 1
+        desc = f"cfg4 fwd+bwd on {batches * 64} of 4096 surfaces ({pts} points), fp64, 1 thread"
+    else:
+        rows = 64
+        w = wl.config5(n_u=8192, n_v=8192)
+        g = rng.standard_normal((1, rows, 8192, 3), dtype=np.float32)
+        a0 = 0
+        while t_used < seconds and a0 + rows <= 8192:
+            u = w.u[a0:a0 + rows]
+            t0 = time.perf_counter()
+            oracle.surface_fwd(w.ctrl, w.U, w.V, u, w.v, w.p, w.q)
+            oracle.surface_bwd(w.ctrl, w.U, w.V, u, w.v, g, w.p, w.q)
+            t_used += time.perf_counter() - t0
+            pts += rows * 8192
+            a0 += rows
+        desc = f"cfg5 fwd+bwd on u-rows [0,{a0}) of 8192 ({pts} points), fp64, 1 thread"
+    return pts / t_used, desc, 1, t_used
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    import workloads as wl
+    oracle.build()
+    rng = np.random.default_rng(7)
+    if args.config == 4:
+        S = 4
+        w = wl.config4(B=S)
+        g = rng.standard_normal((S, 128, 128, 3), dtype=np.float32)
+        u, sample = w.u, f"cfg4: {S} of 4096 surfaces per step (65536 points), fp64 oracle, 1 thread"
+    else:
+        rows = 8
+        w = wl.config5()
+        g = rng.standard_normal((1, rows, 8192, 3), dtype=np.float32)
+        u, sample = w.u[:rows], f"cfg5: {rows} of 8192 u-rows per step ({rows * 8192} points), fp64 oracle, 1 thread"
+    pts = w.B * len(u) * w.n_v
+
+    def step():
+        oracle.surface_fwd(w.ctrl, w.U, w.V, u, w.v, w.p, w.q)
+        oracle.surface_bwd(w.ctrl, w.U, w.V, u, w.v, g, w.p, w.q)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = pts * args.steps / dt
+    line = {"metric": METRIC, "value": value, "unit": "points/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak" if args.config == 4 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(config):
+    if config == 4:
+        return "cfg4: 4096 bicubic NURBS surfaces x 16x16 control nets, 128x128 grid each, fwd+bwd (BASELINE.json configs[3])"
+    return "cfg5: one bicubic 256x256 NURBS surface, 8192x8192 grid, u-rows sharded, fwd+bwd+allreduce (configs[4])"
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_14547_b200 as nb
+    from paper_2104_14547_b200 import dist as nbd
+    import workloads as wl
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    assert args.warmup >= 3, "timing rules need >= 3 warm-up steps"
+
+    hbm_peak, peak_kind = load_peaks()
+    stream = torch.cuda.current_stream()
+
+    # ---------------- inputs (seeded, synthetic, resident in HBM before the timed region)
+    if args.config == 4:
+        w = wl.config4(seed=4 + 1000 * rank)
+        B, n, m, n_u, n_v = w.B, w.n, w.m, w.n_u, w.n_v
+        u_np = w.u
+        a0, a1 = 0, n_u
+    else:
+        w = wl.config5()
+        B, n, m, n_v = w.B, w.n, w.m, w.n_v
+        a0, a1 = nbd.shard_range(w.n_u, world, rank)
+        u_np = w.u[a0:a1]
+        n_u = a1 - a0
+    T = lambda a: torch.from_numpy(a.copy()).to(dev)
+    ctrl, U, V, u, v = T(w.ctrl), T(w.U), T(w.V), T(u_np), T(w.v)
+    sh = nb.nurbs_shape(B, n, m, w.p, w.q, n_u, n_v, 0)
+    tables = nb.Tables.build(sh, U, V, u, v)
+    out = torch.empty((B, n_u, n_v, 3), dtype=torch.float32, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    gout = torch.randn((B, n_u, n_v, 3), dtype=torch.float32, device=dev, generator=gen)
+    gb = nbd.GradBuffer.alloc(B, n, m, U.numel(), V.numel(), dev)
+    ws_bytes = nb.bwd_workspace_bytes(sh)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    launches_per_step = 2 + (1 if ws_bytes > 0 else 0)
+    points = B * n_u * n_v                      # this rank's points per step
+
+    def fwd():
+        nb.nurbs_surface_fwd(sh, ctrl, U, V, u, v, tables, out, stream)
+
+    def bwd():
+        nb.nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, gout, gb.grad_ctrl, gb.grad_U, gb.grad_V, ws,
+                             ws_bytes, stream)
+
+    def reduce():
+        if world > 1 and args.config == 5:
+            nbd.allreduce_grads(gb)
+
+    for _ in range(args.warmup):
+        fwd(); bwd(); reduce()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---------------- timed region: K steps, events between launches on the launching stream
+    K = args.steps
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * K + 1)]
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    with sampler:
+        ev[0].record(stream)
+        for k in range(K):
+            fwd()
+            ev[3 * k + 1].record(stream)
+            bwd()
+            ev[3 * k + 2].record(stream)
+            reduce()
+            ev[3 * k + 3].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = ev[0].elapsed_time(ev[3 * K])
+    fwd_ms = sum(ev[3 * k].elapsed_time(ev[3 * k + 1]) for k in range(K)) / K
+    bwd_ms = sum(ev[3 * k + 1].elapsed_time(ev[3 * k + 2]) for k in range(K)) / K
+    red_ms = sum(ev[3 * k + 2].elapsed_time(ev[3 * k + 3]) for k in range(K)) / K
+    t = torch.tensor([total_ms, fwd_ms, bwd_ms, red_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, fwd_ms, bwd_ms, red_ms = t.tolist()
+    ms_per_step = total_ms / K
+    all_points = points * world if args.config == 4 else w.n_u * n_v
+    value = all_points / (ms_per_step * 1e-3)
+    fwd_value = all_points / (fwd_ms * 1e-3)
+
+    # ---------------- roofline of the dominant kernel (algorithmic bytes)
+    ctrl_bytes = B * n * m * 16
+    tab_bytes = (n_u + n_v) * 20
+    fwd_bytes = points * 12 + ctrl_bytes + tab_bytes
+    bwd_bytes = points * 12 + 2 * ctrl_bytes + tab_bytes + (U.numel() + V.numel()) * 4
+    if bwd_ms >= fwd_ms:
+        kname, kbytes, kms = "nurbs_grid_kernel<3,true> (bwd)", bwd_bytes, bwd_ms
+    else:
+        kname, kbytes, kms = "nurbs_grid_kernel<3,false> (fwd)", fwd_bytes, fwd_ms
+    achieved = kbytes / (kms * 1e-3) / 1e9
+    traffic = load_traffic("bwd" if "bwd" in kname else "fwd", args.config)
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "algorithmic_bytes_per_launch": kbytes,
+                "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                "fwd": {"ms": fwd_ms, "bytes": fwd_bytes, "gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9,
+                        "frac": fwd_bytes / (fwd_ms * 1e-3) / 1e9 / hbm_peak},
+                "bwd": {"ms": bwd_ms, "bytes": bwd_bytes, "gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
+                        "frac": bwd_bytes / (bwd_ms * 1e-3) / 1e9 / hbm_peak}}
+
+    # ---------------- e2e: host buffers through the public API, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_ctrl = ctrl.cpu().pin_memory()
+        h_gout = gout.cpu().pin_memory()
+        h_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+        h_grad = torch.empty(gb.flat.shape, dtype=torch.float32).pin_memory()
+        d_ctrl = torch.empty_like(ctrl)
+        d_gout = torch.empty_like(gout)
+
+        def e2e_step():
+            d_ctrl.copy_(h_ctrl, non_blocking=True)
+            d_gout.copy_(h_gout, non_blocking=True)
+            nb.nurbs_surface_fwd(sh, d_ctrl, U, V, u, v, tables, out, stream)
+            nb.nurbs_surface_bwd(sh, d_ctrl, U, V, u, v, tables, d_gout, gb.grad_ctrl, gb.grad_U, gb.grad_V, ws,
+                                 ws_bytes, stream)
+            reduce()
+            h_out.copy_(out, non_blocking=True)
+            h_grad.copy_(gb.flat, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        E = args.e2e_steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(E):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = te.item() / E
+        h2d = ctrl.numel() * 4 + gout.numel() * 4
+        d2h = out.numel() * 4 + gb.flat.numel() * 4
+        e2e = {"value": all_points / (e2e_ms * 1e-3), "unit": "points/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "note": "pinned host ctrl+grad_out -> device, fwd+bwd via the C ABI, out+grads -> host"}
+
+    # ---------------- oracle cpu baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, desc, cores, used = oracle_rate(args.cpu_seconds, args.config)
+        cpu = {"value": rate, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "seconds": used}
+
+    if rank == 0:
+        clk = sampler.summary()
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "points/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak" if args.config == 4 else "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded lattice+N(0,0.1) control nets, U(0.5,1.5) weights, N(0,1) dL/dS)",
+            "config": {
+                "workload": workload_name(args.config),
+                "global_batch": B * world if args.config == 4 else 1,
+                "points_per_step": all_points,
+                "parallelism": (f"batch-sharded x{world}, no collective" if args.config == 4
+                                else f"u-rows sharded x{world} + NCCL allreduce ({gb.nbytes} B)"),
+                "p": w.p, "q": w.q, "n": n, "m": m, "grid": [w.n_u, n_v],
+                "tables": "precomputed span/basis tables (P:171)",
+                "l2": "inputs larger than L2 (out and dL/dS are 805 MB each), no flush",
+            },
+            "fwd_points_per_s": fwd_value,
+            "fwd_ms": fwd_ms,
+            "bwd_ms": bwd_ms,
+            "allreduce_ms": red_ms if (world > 1 and args.config == 5) else None,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * K,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/*
+ * nurbs.h — C ABI of libnurbs_b200: the data-parallel hot path of NURBS-Diff
+ * (Prasad et al., arXiv 2104.14547) as hand-written sm_100a CUDA.
+ *
+ * Citations: "P:n" = line n of the paper text; "R<k>" = reading k of
+ * DESIGN.md §3 (how a garbled or silent passage is interpreted).
+ *
+ * WHAT IS COMPUTED
+ *   Forward (Eq.2, Eq.3, §3.1.2 steps 1-3 P:138-140, Alg.1):
+ *     S(u_a, v_b) = sum_i sum_j N_i^p(u_a) N_j^q(v_b) w_ij P_ij / sum_i sum_j N_i^p(u_a) N_j^q(v_b) w_ij
+ *     on the tensor grid u[0..n_u) x v[0..n_v) for each of B surfaces (R1: double-sum
+ *     denominator). FindSpan with the half-open interval of P:138 (R2, R3, R4), Cox-de Boor
+ *     (Eq.4) on the p+1 non-zero functions, homogeneous sum and rational
+ *     divide.
+ *   Backward (Eq.8, Eq.9, Eq.10, Alg.2):
+ *     grad_ctrl[k][i][j] = (dL/dx, dL/dy, dL/dz, dL/dw)_ij = sum over points of
+ *     grad_out . dS/dP_ij and grad_out . dS/dw_ij, i.e. J^T (dL/dS). Computed as a
+ *     deterministic transposed banded reduction (no atomics; bitwise repeatable).
+ *     Knot gradients are identically zero by the paper's definition (§3.2.2, R14).
+ *   Curves: the same with the v-direction removed.
+ *
+ * LAYOUT (all fp32, C-contiguous, row-major)
+ *   ctrl      [B][n][m][4]   Cartesian control points and weights (x, y, z, w), w > 0.
+ *   U         [n+p+1]  (knots_batched = 0)  or [B][n+p+1]  (knots_batched = 1); same for V.
+ *             Non-decreasing, U[p] < U[n]; the domain is [U[p], U[n]] (R6).
+ *   u, v      [n_u], [n_v] parameter samples, non-decreasing (the meshgrid of Alg.1, R8),
+ *             inside the domain. Shared by all B surfaces.
+ *   out       [B][n_u][n_v][3]  u-major (R17).
+ *   grad_out  [B][n_u][n_v][3]  dL/dS.
+ *   grad_ctrl [B][n][m][4]  OVERWRITTEN (not accumulated).
+ *   grad_U    [n+p+1] or [B][n+p+1] (nullable) — zero-filled; likewise grad_V.
+ *   Curves: ctrl [B][n][4], U [n+p+1] or [B][n+p+1], u [n_u], out/grad_out [B][n_u][3];
+ *           the shape must have m = 1, q = 0 (n_v is ignored).
+ *
+ * OWNERSHIP AND EXECUTION
+ *   Every tensor pointer is a DEVICE pointer the caller allocates, owns and keeps alive
+ *   until the work queued on `stream` (a cudaStream_t passed as void*, NULL = legacy default
+ *   stream) has completed. Calls enqueue kernels and return immediately; they never
+ *   allocate, free or synchronize, except where stated (nurbs_validate and nurbs_tables
+ *   validate synchronously). Calls are stateless and reentrant across streams.
+ *   Pointers should be 16-byte aligned; otherwise (or if n_v is not a multiple of 4) the
+ *   kernels take a slower non-TMA path with identical results.
+ *
+ * ERRORS
+ *   Every call returns NURBS_OK (0) or an error code; nothing is enqueued on error.
+ *   Shape checks always run on the host. Data checks (knots, parameters, weights live on
+ *   the device) run in nurbs_validate / nurbs_tables, and inside fwd/bwd when the
+ *   environment variable NURBS_CHECK=1 (then those calls synchronize). Unchecked, invalid
+ *   data never causes out-of-bounds access: spans are clamped into [p, n-1].
+ *   nurbs_last_error_detail() returns a thread-local message naming the offending value.
+ */
+#ifndef NURBS_B200_H
+#define NURBS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NURBS_MAX_DEGREE 5
+#define NURBS_ABI_VERSION 1
+
+enum {
+    NURBS_OK = 0,
+    NURBS_E_ARG = 1,          /* null pointer, negative size, n <= p, bad curve shape     */
+    NURBS_E_UNSUPPORTED = 2,  /* degree outside 1..NURBS_MAX_DEGREE                       */
+    NURBS_E_KNOTS = 3,        /* knots decreasing, or empty domain U[p] == U[n]           */
+    NURBS_E_DOMAIN = 4,       /* a parameter outside [U[p], U[n]]                  */
+    NURBS_E_WEIGHT = 5,       /* a weight w <= 0 (R15) or non-finite input                */
+    NURBS_E_UNSORTED = 6,     /* u or v not non-decreasing                                */
+    NURBS_E_CUDA = 7,         /* a CUDA runtime error (detail names it)                   */
+    NURBS_E_WORKSPACE = 8,    /* workspace NULL or smaller than nurbs_*_workspace_bytes   */
+    NURBS_E_TABLES = 9        /* tables given with knots_batched = 1, or mismatched header */
+};
+
+typedef struct {
+    int32_t B;              /* batch of surfaces (or curves)                              */
+    int32_t n, m;           /* control-point COUNTS in u, v (curve: m = 1)   (R6)         */
+    int32_t p, q;           /* degrees 1..NURBS_MAX_DEGREE (curve: q = 0)                 */
+    int32_t n_u, n_v;       /* parameter samples; the grid is n_u x n_v (curve: n_v unused)*/
+    int32_t knots_batched;  /* 0: U, V shared by the batch; 1: one knot vector per item   */
+} nurbs_shape;
+
+/* ---------------------------------------------------------------------------------------
+ * Span/basis tables — the "pre-compute the knot spans and basis functions during the
+ * initialization of the NURBS layer" of P:171 (and the stored u_span, N_i of Alg.1).
+ * Valid for one (shape.n, m, p, q, n_u, n_v), one knot pair U, V (knots_batched must be 0)
+ * and one sample pair u, v. `tables` is caller-allocated DEVICE memory of
+ * nurbs_tables_bytes(shape) bytes, 16-byte aligned. nurbs_tables validates U, V, u, v
+ * (synchronizing once) and fills the tables on `stream`. Passing tables to fwd/bwd is
+ * optional (NULL = compute spans and bases in-kernel); results are identical.
+ * For curves pass the curve shape (m = 1, q = 0) and V = v = NULL.
+ * --------------------------------------------------------------------------------------- */
+size_t nurbs_tables_bytes(const nurbs_shape* shape);
+int    nurbs_tables(const nurbs_shape* shape, const float* U, const float* V,
+                    const float* u, const float* v, void* tables, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Surfaces. nurbs_surface_fwd: Eq.3 on the grid. nurbs_surface_bwd: J^T grad_out
+ * (Eq.8/9/10), grad_ctrl overwritten, grad_U/grad_V zero-filled if non-NULL.
+ * The backward needs a DEVICE workspace of nurbs_surface_bwd_workspace_bytes(shape) bytes
+ * (0 is possible: then workspace may be NULL) for the fixed-order cross-tile reduction.
+ * --------------------------------------------------------------------------------------- */
+int    nurbs_surface_fwd(const nurbs_shape* shape, const float* ctrl,
+                         const float* U, const float* V, const float* u, const float* v,
+                         const void* tables, float* out, void* stream);
+int    nurbs_surface_bwd(const nurbs_shape* shape, const float* ctrl,
+                         const float* U, const float* V, const float* u, const float* v,
+                         const void* tables, const float* grad_out,
+                         float* grad_ctrl, float* grad_U, float* grad_V,
+                         void* workspace, size_t ws_bytes, void* stream);
+size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* shape);
+
+/* ---------------------------------------------------------------------------------------
+ * Curves: shape.m = 1, shape.q = 0. Same semantics as the surface calls.
+ * --------------------------------------------------------------------------------------- */
+int    nurbs_curve_fwd(const nurbs_shape* shape, const float* ctrl, const float* U,
+                       const float* u, const void* tables, float* out, void* stream);
+int    nurbs_curve_bwd(const nurbs_shape* shape, const float* ctrl, const float* U,
+                       const float* u, const void* tables, const float* grad_out,
+                       float* grad_ctrl, float* grad_U,
+                       void* workspace, size_t ws_bytes, void* stream);
+size_t nurbs_curve_bwd_workspace_bytes(const nurbs_shape* shape);
+
+/* ---------------------------------------------------------------------------------------
+ * Checked mode. nurbs_validate checks every data precondition (knots non-decreasing and
+ * non-empty domain, u/v sorted and inside the domain, weights > 0 and finite) on `stream`
+ * and SYNCHRONIZES; returns the first error found. Curves: V = v = NULL with the curve shape.
+ * --------------------------------------------------------------------------------------- */
+int         nurbs_validate(const nurbs_shape* shape, const float* ctrl, const float* U,
+                           const float* V, const float* u, const float* v, void* stream);
+const char* nurbs_strerror(int status);
+const char* nurbs_last_error_detail(void);
+int         nurbs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NURBS_B200_H */

@@ -1,0 +1,158 @@
+"""Python binding of include/nurbs.h: same names as the C ABI, torch tensors as device
+memory. Argument marshalling only — every step of the path runs in libnurbs_b200.so.
+
+Low-level calls (``nurbs_surface_fwd`` ...) take a ``nurbs_shape`` and tensors (or raw
+device addresses as ints) exactly like the C functions; ``stream`` defaults to torch's
+current CUDA stream. Convenience wrappers (``surface_fwd`` ...) infer the shape and allocate
+outputs with torch.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from ._abi import check, load, nurbs_shape
+
+_F32 = torch.float32
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    if isinstance(x, torch.Tensor):
+        if not x.is_cuda:
+            raise ValueError("libnurbs_b200 takes device tensors (CUDA); got a CPU tensor")
+        if not x.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return ctypes.c_void_p(x.data_ptr())
+    if isinstance(x, Tables):
+        return ctypes.c_void_p(x.buf.data_ptr())
+    raise TypeError(f"cannot pass {type(x)} as a device pointer")
+
+
+def _stream(stream):
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+# ----------------------------------------------------------------------------- shapes
+def surface_shape(ctrl: torch.Tensor, U: torch.Tensor, u: torch.Tensor, v: torch.Tensor,
+                  p: int, q: int) -> nurbs_shape:
+    B, n, m, four = ctrl.shape
+    assert four == 4, "ctrl must be [B][n][m][4]"
+    return nurbs_shape(B, n, m, p, q, u.numel(), v.numel(), 1 if U.dim() == 2 else 0)
+
+
+def curve_shape(ctrl: torch.Tensor, U: torch.Tensor, u: torch.Tensor, p: int) -> nurbs_shape:
+    B, n, four = ctrl.shape
+    assert four == 4, "ctrl must be [B][n][4]"
+    return nurbs_shape(B, n, 1, p, 0, u.numel(), 1, 1 if U.dim() == 2 else 0)
+
+
+def _is_curve(sh: nurbs_shape) -> bool:
+    return sh.m == 1 and sh.q == 0
+
+
+def bwd_workspace_bytes(sh: nurbs_shape) -> int:
+    L = load()
+    f = L.nurbs_curve_bwd_workspace_bytes if _is_curve(sh) else L.nurbs_surface_bwd_workspace_bytes
+    return int(f(ctypes.byref(sh)))
+
+
+# ----------------------------------------------------------------------------- C ABI mirror
+def nurbs_tables(sh, U, V, u, v, tables, stream=None):
+    check(load().nurbs_tables(ctypes.byref(sh), _ptr(U), _ptr(V), _ptr(u), _ptr(v), _ptr(tables),
+                              _stream(stream)), "nurbs_tables")
+
+
+def nurbs_surface_fwd(sh, ctrl, U, V, u, v, tables, out, stream=None):
+    check(load().nurbs_surface_fwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
+                                   _ptr(tables), _ptr(out), _stream(stream)), "nurbs_surface_fwd")
+
+
+def nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, grad_U, grad_V,
+                      workspace, ws_bytes, stream=None):
+    check(load().nurbs_surface_bwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
+                                   _ptr(tables), _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U),
+                                   _ptr(grad_V), _ptr(workspace), ctypes.c_size_t(ws_bytes),
+                                   _stream(stream)), "nurbs_surface_bwd")
+
+
+def nurbs_curve_fwd(sh, ctrl, U, u, tables, out, stream=None):
+    check(load().nurbs_curve_fwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(u), _ptr(tables), _ptr(out),
+                                 _stream(stream)), "nurbs_curve_fwd")
+
+
+def nurbs_curve_bwd(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspace, ws_bytes, stream=None):
+    check(load().nurbs_curve_bwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(u), _ptr(tables),
+                                 _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U), _ptr(workspace),
+                                 ctypes.c_size_t(ws_bytes), _stream(stream)), "nurbs_curve_bwd")
+
+
+def nurbs_validate(sh, ctrl, U, V, u, v, stream=None):
+    check(load().nurbs_validate(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
+                                _stream(stream)), "nurbs_validate")
+
+
+# ----------------------------------------------------------------------------- tables
+@dataclass
+class Tables:
+    """Span/basis tables for fixed knots and a fixed parameter grid (P:171 precompute)."""
+    shape: nurbs_shape
+    buf: torch.Tensor
+
+    @staticmethod
+    def build(sh: nurbs_shape, U, V, u, v, stream=None) -> "Tables":
+        nbytes = int(load().nurbs_tables_bytes(ctypes.byref(sh)))
+        dev = (U if isinstance(U, torch.Tensor) else u).device
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        nurbs_tables(sh, U, V, u, v, buf, stream)
+        return Tables(sh, buf)
+
+
+# ----------------------------------------------------------------------------- wrappers
+def surface_fwd(ctrl, U, V, u, v, p: int, q: int, tables: Tables | None = None, out=None, stream=None):
+    sh = surface_shape(ctrl, U, u, v, p, q)
+    if out is None:
+        out = torch.empty((sh.B, sh.n_u, sh.n_v, 3), dtype=_F32, device=ctrl.device)
+    nurbs_surface_fwd(sh, ctrl, U, V, u, v, tables, out, stream)
+    return out
+
+
+def surface_bwd(ctrl, U, V, u, v, grad_out, p: int, q: int, tables: Tables | None = None,
+                grad_ctrl=None, grad_U=None, grad_V=None, workspace=None, stream=None):
+    sh = surface_shape(ctrl, U, u, v, p, q)
+    if grad_ctrl is None:
+        grad_ctrl = torch.empty_like(ctrl)
+    ws = bwd_workspace_bytes(sh)
+    if workspace is None and ws > 0:
+        workspace = torch.empty(ws, dtype=torch.uint8, device=ctrl.device)
+    nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws, stream)
+    return grad_ctrl
+
+
+def curve_fwd(ctrl, U, u, p: int, tables: Tables | None = None, out=None, stream=None):
+    sh = curve_shape(ctrl, U, u, p)
+    if out is None:
+        out = torch.empty((sh.B, sh.n_u, 3), dtype=_F32, device=ctrl.device)
+    nurbs_curve_fwd(sh, ctrl, U, u, tables, out, stream)
+    return out
+
+
+def curve_bwd(ctrl, U, u, grad_out, p: int, tables: Tables | None = None, grad_ctrl=None, grad_U=None,
+              workspace=None, stream=None):
+    sh = curve_shape(ctrl, U, u, p)
+    if grad_ctrl is None:
+        grad_ctrl = torch.empty_like(ctrl)
+    ws = bwd_workspace_bytes(sh)
+    if workspace is None and ws > 0:
+        workspace = torch.empty(ws, dtype=torch.uint8, device=ctrl.device)
+    nurbs_curve_bwd(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspace, ws, stream)
+    return grad_ctrl

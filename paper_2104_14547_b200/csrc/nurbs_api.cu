@@ -1,0 +1,345 @@
+// nurbs_api.cu — host side of the C ABI declared in include/nurbs.h: shape checks, the
+// launch plan, checked mode, and the kernel launches on the caller's stream.
+// Citations: P:n = reference/PAPER.md line n; R<k> = DESIGN.md §3 reading k.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/nurbs.h"
+#include "nurbs_internal.cuh"
+
+using nb::Dir;
+using nb::Params;
+using nb::Plan;
+
+namespace {
+
+thread_local std::string g_detail;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_detail = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(NURBS_E_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool check_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* s = getenv("NURBS_CHECK");
+    mode = (s && s[0] && s[0] != '0') ? 1 : 0;
+  }
+  return mode == 1;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Shape rules shared by surfaces and curves (one direction).
+int check_dir(const char* name, int n, int p, int ns) {
+  if (p < 1 || p > NURBS_MAX_DEGREE) return fail(NURBS_E_UNSUPPORTED, "%s: degree %d outside 1..%d", name, p, NURBS_MAX_DEGREE);
+  if (n <= p) return fail(NURBS_E_ARG, "%s: control count %d must exceed degree %d", name, n, p);
+  if (ns < 0) return fail(NURBS_E_ARG, "%s: negative sample count %d", name, ns);
+  return NURBS_OK;
+}
+
+int check_surface_shape(const nurbs_shape* sh) {
+  if (!sh) return fail(NURBS_E_ARG, "shape is NULL");
+  if (sh->B < 0) return fail(NURBS_E_ARG, "negative batch %d", sh->B);
+  if (sh->knots_batched != 0 && sh->knots_batched != 1) return fail(NURBS_E_ARG, "knots_batched must be 0 or 1");
+  int st = check_dir("u", sh->n, sh->p, sh->n_u);
+  if (st) return st;
+  return check_dir("v", sh->m, sh->q, sh->n_v);
+}
+
+int check_curve_shape(const nurbs_shape* sh) {
+  if (!sh) return fail(NURBS_E_ARG, "shape is NULL");
+  if (sh->B < 0) return fail(NURBS_E_ARG, "negative batch %d", sh->B);
+  if (sh->m != 1 || sh->q != 0) return fail(NURBS_E_ARG, "curve shape needs m = 1, q = 0 (got m=%d q=%d)", sh->m, sh->q);
+  if (sh->knots_batched != 0 && sh->knots_batched != 1) return fail(NURBS_E_ARG, "knots_batched must be 0 or 1");
+  return check_dir("u", sh->n, sh->p, sh->n_u);
+}
+
+// Internal directions. Surfaces: rows = u, cols = v. Curves: rows trivial, cols = the curve.
+struct Geo {
+  int B, P;
+  Dir r, c;
+};
+
+Geo surface_geo(const nurbs_shape* sh, const float* U, const float* V, const float* u, const float* v) {
+  Geo g{};
+  g.B = sh->B;
+  g.P = sh->p;
+  g.r = Dir{sh->n, sh->p, sh->n_u, U, sh->knots_batched ? (long long)(sh->n + sh->p + 1) : 0LL, u, nullptr, nullptr, 0};
+  g.c = Dir{sh->m, sh->q, sh->n_v, V, sh->knots_batched ? (long long)(sh->m + sh->q + 1) : 0LL, v, nullptr, nullptr, 0};
+  return g;
+}
+
+Geo curve_geo(const nurbs_shape* sh, const float* U, const float* u) {
+  Geo g{};
+  g.B = sh->B;
+  g.P = 0;
+  g.r = Dir{1, 0, 1, nullptr, 0, nullptr, nullptr, nullptr, 0};
+  g.c = Dir{sh->n, sh->p, sh->n_u, U, sh->knots_batched ? (long long)(sh->n + sh->p + 1) : 0LL, u, nullptr, nullptr, 0};
+  return g;
+}
+
+void attach_tables(Geo& g, const void* tables) {
+  if (!tables) return;
+  const nb::TabLayout L = nb::tab_layout(g.P > 0 ? g.r.ns : 0, g.r.p, g.c.ns, g.c.p);
+  const unsigned char* t = static_cast<const unsigned char*>(tables);
+  if (g.P > 0) {
+    g.r.tspan = reinterpret_cast<const int*>(t + L.off_span_r);
+    g.r.tN = reinterpret_cast<const float*>(t + L.off_N_r);
+    g.r.tnp = L.np_r;
+  }
+  g.c.tspan = reinterpret_cast<const int*>(t + L.off_span_c);
+  g.c.tN = reinterpret_cast<const float*>(t + L.off_N_c);
+  g.c.tnp = L.np_c;
+}
+
+// Checked mode: validate data on the device and synchronize.
+int validate_geo(const Geo& g, const float* ctrl, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return cuda_fail(e, "validate: cudaMallocAsync");
+  e = cudaMemsetAsync(d, 0xff, sizeof(unsigned long long), st);
+  if (e == cudaSuccess)
+    e = nb::launch_validate(g.B, g.r, g.c, g.P > 0, reinterpret_cast<const float4*>(ctrl),
+                            (long long)g.B * g.r.n * g.c.n, d, st);
+  unsigned long long h = ~0ull;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(d, st);
+  if (e != cudaSuccess) return cuda_fail(e, "validate");
+  if (h == ~0ull) return NURBS_OK;
+  const int code = (int)(h >> 48);
+  const int which = (int)((h >> 40) & 0xff);
+  const long long idx = (long long)(h & 0xffffffffffull);
+  static const char* names[] = {"ctrl (weight <= 0 or non-finite)", "row-direction knots", "column-direction knots",
+                                "row-direction samples", "column-direction samples"};
+  return fail(code, "invalid %s at flat index %lld", which < 5 ? names[which] : "?", idx);
+}
+
+int launch(const Geo& g, bool bwd, const float* ctrl, float* out, const float* gout, float* gctrl, float* gR,
+           float* gC, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns);
+  const size_t grad_bytes = (size_t)g.B * g.r.n * g.c.n * 16;
+  const int gR_per = g.r.n + g.r.p + 1, gC_per = g.c.n + g.c.p + 1;
+  const int gR_items = g.r.kstride ? g.B : 1, gC_items = g.c.kstride ? g.B : 1;
+  if (g.B == 0) return NURBS_OK;
+  if (g.r.ns == 0 || g.c.ns == 0) {
+    if (!bwd) return NURBS_OK;
+    cudaError_t e = cudaMemsetAsync(gctrl, 0, grad_bytes, st);
+    if (e == cudaSuccess && gR) e = cudaMemsetAsync(gR, 0, sizeof(float) * (size_t)gR_per * gR_items, st);
+    if (e == cudaSuccess && gC) e = cudaMemsetAsync(gC, 0, sizeof(float) * (size_t)gC_per * gC_items, st);
+    return e == cudaSuccess ? NURBS_OK : cuda_fail(e, "zero-fill");
+  }
+  if (pl.grid > 0x7fffffffLL) return fail(NURBS_E_ARG, "grid of %lld CTAs too large", pl.grid);
+  if (bwd && pl.ws_bytes > 0) {
+    if (!ws || ws_bytes < pl.ws_bytes)
+      return fail(NURBS_E_WORKSPACE, "backward needs a %zu-byte workspace (got %zu at %p)", pl.ws_bytes, ws_bytes, ws);
+  }
+  Params prm{};
+  prm.B = g.B;
+  prm.r = g.r;
+  prm.c = g.c;
+  prm.ctrl = reinterpret_cast<const float4*>(ctrl);
+  prm.out = out;
+  prm.gout = gout;
+  prm.gctrl = reinterpret_cast<float4*>(gctrl);
+  prm.gR = gR;
+  prm.gR_per = gR_per;
+  prm.gR_items = gR_items;
+  prm.gC = gC;
+  prm.gC_per = gC_per;
+  prm.gC_items = gC_items;
+  prm.K = pl.K;
+  prm.NRB = pl.NRB;
+  prm.NCB = pl.NCB;
+  prm.T_rows = pl.T_rows;
+  prm.direct = pl.direct;
+  const void* io = bwd ? static_cast<const void*>(gout) : static_cast<const void*>(out);
+  prm.bulk = (g.c.ns % 4 == 0) && aligned16(io) ? 1 : 0;
+  if (getenv("NURBS_NO_TMA")) prm.bulk = 0;
+  if (bwd && !pl.direct) {
+    prm.slots = reinterpret_cast<float4*>(ws);
+    prm.colband = reinterpret_cast<int2*>(static_cast<unsigned char*>(ws) + pl.slots_bytes);
+  }
+  cudaError_t e = nb::launch_grid(prm, bwd, g.P, g.c.p, st);
+  if (e != cudaSuccess) return cuda_fail(e, bwd ? "backward kernel launch" : "forward kernel launch");
+  if (bwd && !pl.direct) {
+    e = nb::launch_reduce(prm, g.P, st);
+    if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
+  }
+  return NURBS_OK;
+}
+
+int check_ptrs(bool bwd, const void* ctrl, const void* out, const void* gout, const void* gctrl) {
+  if (!ctrl) return fail(NURBS_E_ARG, "ctrl is NULL");
+  if (!bwd && !out) return fail(NURBS_E_ARG, "out is NULL");
+  if (bwd && !gout) return fail(NURBS_E_ARG, "grad_out is NULL");
+  if (bwd && !gctrl) return fail(NURBS_E_ARG, "grad_ctrl is NULL");
+  if (!aligned16(ctrl)) return fail(NURBS_E_ARG, "ctrl must be 16-byte aligned (float4 control points)");
+  if (bwd && !aligned16(gctrl)) return fail(NURBS_E_ARG, "grad_ctrl must be 16-byte aligned");
+  return NURBS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nurbs_abi_version(void) { return NURBS_ABI_VERSION; }
+
+const char* nurbs_strerror(int status) {
+  switch (status) {
+    case NURBS_OK: return "ok";
+    case NURBS_E_ARG: return "invalid argument";
+    case NURBS_E_UNSUPPORTED: return "unsupported degree";
+    case NURBS_E_KNOTS: return "invalid knot vector";
+    case NURBS_E_DOMAIN: return "parameter outside the knot domain";
+    case NURBS_E_WEIGHT: return "invalid weight or non-finite control point";
+    case NURBS_E_UNSORTED: return "parameters not sorted";
+    case NURBS_E_CUDA: return "CUDA error";
+    case NURBS_E_WORKSPACE: return "workspace missing or too small";
+    case NURBS_E_TABLES: return "tables unusable for this call";
+    default: return "unknown status";
+  }
+}
+
+const char* nurbs_last_error_detail(void) { return g_detail.c_str(); }
+
+size_t nurbs_tables_bytes(const nurbs_shape* sh) {
+  if (!sh) return 0;
+  if (sh->m == 1 && sh->q == 0) return nb::tab_layout(0, 0, sh->n_u, sh->p).bytes;
+  return nb::tab_layout(sh->n_u, sh->p, sh->n_v, sh->q).bytes;
+}
+
+int nurbs_tables(const nurbs_shape* sh, const float* U, const float* V, const float* u, const float* v,
+                 void* tables, void* stream) {
+  g_detail.clear();
+  const bool curve = sh && sh->m == 1 && sh->q == 0;
+  int st = curve ? check_curve_shape(sh) : check_surface_shape(sh);
+  if (st) return st;
+  if (sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  if (!tables || !U || !u || (!curve && (!V || !v))) return fail(NURBS_E_ARG, "NULL pointer");
+  if (!aligned16(tables)) return fail(NURBS_E_ARG, "tables must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = curve ? curve_geo(sh, U, u) : surface_geo(sh, U, V, u, v);
+  g.B = 1;
+  // validate knots and samples (weights are not part of the tables)
+  {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return cuda_fail(e, "tables: cudaMallocAsync");
+    e = cudaMemsetAsync(d, 0xff, sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = nb::launch_validate(1, g.r, g.c, !curve, nullptr, 0, d, s);
+    unsigned long long h = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(d, s);
+    if (e != cudaSuccess) return cuda_fail(e, "tables: validate");
+    if (h != ~0ull) return fail((int)(h >> 48), "tables: invalid knots or samples (flat index %lld)", (long long)(h & 0xffffffffffull));
+  }
+  Dir r = g.r;
+  if (curve) r.ns = 0;
+  const nb::TabLayout L = nb::tab_layout(r.ns, r.p, g.c.ns, g.c.p);
+  cudaError_t e = nb::launch_tables(r, g.c, tables, L, s);
+  if (e != cudaSuccess) return cuda_fail(e, "tables kernel launch");
+  return NURBS_OK;
+}
+
+size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* sh) {
+  if (!sh || sh->B <= 0) return 0;
+  return nb::make_plan(sh->B, sh->n, sh->p, sh->n_u, sh->m, sh->n_v).ws_bytes;
+}
+
+size_t nurbs_curve_bwd_workspace_bytes(const nurbs_shape* sh) {
+  if (!sh || sh->B <= 0) return 0;
+  return nb::make_plan(sh->B, 1, 0, 1, sh->n, sh->n_u).ws_bytes;
+}
+
+int nurbs_validate(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* u,
+                   const float* v, void* stream) {
+  g_detail.clear();
+  const bool curve = sh && sh->m == 1 && sh->q == 0;
+  int st = curve ? check_curve_shape(sh) : check_surface_shape(sh);
+  if (st) return st;
+  if (!ctrl || !U || !u || (!curve && (!V || !v))) return fail(NURBS_E_ARG, "NULL pointer");
+  Geo g = curve ? curve_geo(sh, U, u) : surface_geo(sh, U, V, u, v);
+  return validate_geo(g, ctrl, static_cast<cudaStream_t>(stream));
+}
+
+int nurbs_surface_fwd(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* u,
+                      const float* v, const void* tables, float* out, void* stream) {
+  g_detail.clear();
+  int st = check_surface_shape(sh);
+  if (st) return st;
+  if ((st = check_ptrs(false, ctrl, out, nullptr, nullptr))) return st;
+  if (!tables && (!U || !V || !u || !v)) return fail(NURBS_E_ARG, "NULL knots or samples");
+  if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = surface_geo(sh, U, V, u, v);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  attach_tables(g, tables);
+  return launch(g, false, ctrl, out, nullptr, nullptr, nullptr, nullptr, nullptr, 0, s);
+}
+
+int nurbs_surface_bwd(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* u,
+                      const float* v, const void* tables, const float* grad_out, float* grad_ctrl, float* grad_U,
+                      float* grad_V, void* workspace, size_t ws_bytes, void* stream) {
+  g_detail.clear();
+  int st = check_surface_shape(sh);
+  if (st) return st;
+  if ((st = check_ptrs(true, ctrl, nullptr, grad_out, grad_ctrl))) return st;
+  if (!tables && (!U || !V || !u || !v)) return fail(NURBS_E_ARG, "NULL knots or samples");
+  if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = surface_geo(sh, U, V, u, v);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  attach_tables(g, tables);
+  return launch(g, true, ctrl, nullptr, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes, s);
+}
+
+int nurbs_curve_fwd(const nurbs_shape* sh, const float* ctrl, const float* U, const float* u, const void* tables,
+                    float* out, void* stream) {
+  g_detail.clear();
+  int st = check_curve_shape(sh);
+  if (st) return st;
+  if ((st = check_ptrs(false, ctrl, out, nullptr, nullptr))) return st;
+  if (!tables && (!U || !u)) return fail(NURBS_E_ARG, "NULL knots or samples");
+  if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = curve_geo(sh, U, u);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  attach_tables(g, tables);
+  return launch(g, false, ctrl, out, nullptr, nullptr, nullptr, nullptr, nullptr, 0, s);
+}
+
+int nurbs_curve_bwd(const nurbs_shape* sh, const float* ctrl, const float* U, const float* u, const void* tables,
+                    const float* grad_out, float* grad_ctrl, float* grad_U, void* workspace, size_t ws_bytes,
+                    void* stream) {
+  g_detail.clear();
+  int st = check_curve_shape(sh);
+  if (st) return st;
+  if ((st = check_ptrs(true, ctrl, nullptr, grad_out, grad_ctrl))) return st;
+  if (!tables && (!U || !u)) return fail(NURBS_E_ARG, "NULL knots or samples");
+  if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = curve_geo(sh, U, u);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  attach_tables(g, tables);
+  return launch(g, true, ctrl, nullptr, grad_out, grad_ctrl, nullptr, grad_U, workspace, ws_bytes, s);
+}
+
+}  // extern "C"

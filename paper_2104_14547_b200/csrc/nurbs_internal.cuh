@@ -1,0 +1,122 @@
+// nurbs_internal.cuh — structures shared by the sm_100a kernels (nurbs_kernels.cu) and the
+// host C ABI (nurbs_api.cu). Not part of the public ABI (include/nurbs.h).
+//
+// Vocabulary: the kernels work on an internal "rows x cols" grid. For a surface, rows = the
+// u direction (control count n, degree p, samples u) and cols = the v direction (m, q, v).
+// A curve is the same grid with a trivial row direction (one control row, degree 0,
+// one sample) and the curve along the columns.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nb {
+
+constexpr int kCB = 128;          // sample columns per CTA block = compute threads
+constexpr int kCompute = 128;     // compute threads (4 warps)
+constexpr int kThreads = 160;     // + 1 producer warp issuing TMA bulk copies
+constexpr int kRPS = 4;           // sample rows per pipeline stage
+constexpr int kStages = 3;        // pipeline depth (stage ring)
+constexpr int kRowChunk = 64;     // rows whose span/basis are staged in smem at once
+constexpr int kMaxQ = 5;          // max column degree (runtime q)
+constexpr int kRMax = 16;         // max control rows in a row-block band (T/H smem rows)
+constexpr int kTargetCTAs = 592;  // 4 resident CTAs x 148 SMs: planning target (fixed so the
+                                  // plan, hence summation order, is a pure function of shape)
+
+// One parametric direction.
+struct Dir {
+  int n;                    // control-point count
+  int p;                    // degree (rows: template P; cols: runtime q)
+  int ns;                   // number of samples
+  const float* knots;       // [n+p+1] or batched
+  long long kstride;        // floats between batch items' knot vectors (0 = shared)
+  const float* s;           // samples [ns]
+  const int* tspan;         // optional tables: span per sample
+  const float* tN;          // optional tables: basis per sample, tnp floats each
+  int tnp;
+};
+
+struct Params {
+  int B;
+  Dir r, c;
+  const float4* ctrl;       // [B][r.n][c.n] (x,y,z,w)
+  float* out;               // [B][r.ns][c.ns][3]
+  const float* gout;        // [B][r.ns][c.ns][3]
+  float4* gctrl;            // [B][r.n][c.n]
+  float* gR; int gR_per; int gR_items;   // knot-gradient zero fill (rows direction)
+  float* gC; int gC_per; int gC_items;   // (cols direction)
+  int K;                    // knot spans per row block
+  int NRB, NCB;             // row blocks, column blocks
+  int T_rows;               // smem rows of T/H = slot rows
+  int bulk;                 // 1: TMA bulk staging of out / grad_out
+  int direct;               // 1: bwd writes grad_ctrl in-kernel (NRB == NCB == 1)
+  float4* slots;            // [B][NRB][NCB][T_rows][c.n] partial dQ (direct == 0)
+  int2* colband;            // [B][NCB] (j0, j1) column band of each column block
+};
+
+// Tables blob layout (nurbs_tables): header then four arrays, each 256-byte aligned.
+struct TabLayout {
+  size_t off_span_r, off_N_r, off_span_c, off_N_c, bytes;
+  int np_r, np_c;
+};
+
+inline int basis_stride(int p) { return (p + 1) <= 4 ? 4 : 8; }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline TabLayout tab_layout(int ns_r, int p_r, int ns_c, int p_c) {
+  TabLayout L;
+  L.np_r = basis_stride(p_r);
+  L.np_c = basis_stride(p_c);
+  size_t o = 256;  // header
+  L.off_span_r = o; o = align_up(o + sizeof(int) * (size_t)ns_r, 256);
+  L.off_N_r = o;    o = align_up(o + sizeof(float) * (size_t)ns_r * L.np_r, 256);
+  L.off_span_c = o; o = align_up(o + sizeof(int) * (size_t)ns_c, 256);
+  L.off_N_c = o;    o = align_up(o + sizeof(float) * (size_t)ns_c * L.np_c, 256);
+  L.bytes = o;
+  return L;
+}
+
+constexpr uint32_t kTabMagic = 0x4e524253u;  // "NRBS"
+
+struct Plan {
+  int K, NRB, NCB, T_rows, direct;
+  long long grid;
+  size_t slots_bytes, colband_bytes, ws_bytes;
+};
+
+inline Plan make_plan(int B, int n_r, int P, int ns_r, int n_c, int ns_c) {
+  Plan pl{};
+  const int spans = n_r - P;
+  pl.NCB = (ns_c + kCB - 1) / kCB;
+  int K = spans;
+  if (K + P > kRMax) K = kRMax - P;
+  if (K < 1) K = 1;
+  while (K > 1 && (long long)B * ((spans + K - 1) / K) * pl.NCB < kTargetCTAs) K = (K + 1) / 2;
+  pl.K = K;
+  pl.NRB = (spans + K - 1) / K;
+  pl.T_rows = (K + P < n_r) ? (K + P) : n_r;
+  pl.direct = (pl.NRB == 1 && pl.NCB == 1) ? 1 : 0;
+  pl.grid = (long long)B * pl.NRB * pl.NCB;
+  if (pl.direct || B == 0 || ns_r == 0 || ns_c == 0) {
+    pl.slots_bytes = pl.colband_bytes = pl.ws_bytes = 0;
+  } else {
+    pl.slots_bytes = align_up((size_t)B * pl.NRB * pl.NCB * pl.T_rows * (size_t)n_c * 16, 256);
+    pl.colband_bytes = align_up((size_t)B * pl.NCB * sizeof(int2), 256);
+    pl.ws_bytes = pl.slots_bytes + pl.colband_bytes;
+  }
+  (void)ns_r;
+  return pl;
+}
+
+// Launchers (nurbs_kernels.cu). Return cudaError_t of the launch.
+cudaError_t launch_grid(const Params& prm, bool bwd, int P, int q, cudaStream_t st);
+cudaError_t launch_reduce(const Params& prm, int P, cudaStream_t st);
+cudaError_t launch_tables(const Dir& r, const Dir& c, void* tables, const TabLayout& L,
+                          cudaStream_t st);
+// status: device buffer of one unsigned long long, pre-set to ~0ull.
+cudaError_t launch_validate(int B, const Dir& r, const Dir& c, int check_rows,
+                            const float4* ctrl, long long n_ctrl,
+                            unsigned long long* status, cudaStream_t st);
+size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows);
+
+}  // namespace nb

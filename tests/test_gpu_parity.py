@@ -1,0 +1,347 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on the same
+seeded fp32 inputs. Tolerances (north_star, normwise per reading R16 of DESIGN.md §3):
+  spans / indices      bit-exact
+  forward              max|S_gpu - S_ref| / max|P|          <= 1e-5  per surface
+  gradients            max|d_gpu - d_ref| / max|d_ref|      <= 1e-4  per tensor (dP, dw) per surface
+  knot gradients       exactly zero
+  repeatability        bitwise
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_14547_b200 as nb  # noqa: E402
+from paper_2104_14547_b200 import _abi  # noqa: E402
+
+DEV = torch.device("cuda:0")
+FWD_TOL, BWD_TOL = 1e-5, 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2104_14547_b200.build import build
+    build()
+    oracle.build()
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def fwd_err(gpu, ref, ctrl):
+    """per-surface normwise forward error"""
+    B = ctrl.shape[0]
+    e = np.abs(gpu.reshape(B, -1) - ref.reshape(B, -1)).max(axis=1)
+    scale = np.abs(ctrl[..., :3].reshape(B, -1)).max(axis=1)
+    return float(np.max(e / scale))
+
+
+def bwd_err(gpu, ref):
+    """max over surfaces and over the two tensors (dP, dw) of max|diff| / max|ref|"""
+    B = ref.shape[0]
+    worst = 0.0
+    for sl in (np.s_[..., :3], np.s_[..., 3]):
+        g, r = gpu[sl].reshape(B, -1), ref[sl].reshape(B, -1)
+        sc = np.abs(r).max(axis=1)
+        sc[sc == 0] = 1.0
+        worst = max(worst, float(np.max(np.abs(g - r).max(axis=1) / sc)))
+    return worst
+
+
+def run_surface(w, g, tables=False, grad_knots=True):
+    ctrl, U, V, u, v, gout = T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v), T(g)
+    tab = None
+    if tables:
+        sh = nb.surface_shape(ctrl, U, u, v, w.p, w.q)
+        tab = nb.Tables.build(sh, U, V, u, v)
+    out = nb.surface_fwd(ctrl, U, V, u, v, w.p, w.q, tables=tab)
+    gU = torch.full_like(U, 3.0) if grad_knots else None
+    gV = torch.full_like(V, -2.0) if grad_knots else None
+    grad = nb.surface_bwd(ctrl, U, V, u, v, gout, w.p, w.q, tables=tab, grad_U=gU, grad_V=gV)
+    torch.cuda.synchronize()
+    if grad_knots:
+        assert torch.all(gU == 0) and torch.all(gV == 0)
+    return out.cpu().numpy(), grad.cpu().numpy()
+
+
+def check_surface(w, gseed=0, tables=False, fwd_tol=FWD_TOL, bwd_tol=BWD_TOL):
+    g = w.grad_out(gseed)
+    out, grad = run_surface(w, g, tables)
+    ref_out = oracle.surface_fwd(w.ctrl, w.U, w.V, w.u, w.v, w.p, w.q, w.knots_batched)
+    ref_grad = oracle.surface_bwd(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q, w.knots_batched)
+    ef, eb = fwd_err(out, ref_out, w.ctrl), bwd_err(grad, ref_grad)
+    assert ef <= fwd_tol, f"{w.name}: forward error {ef:.3e}"
+    assert eb <= bwd_tol, f"{w.name}: backward error {eb:.3e}"
+    return ef, eb
+
+
+# --------------------------------------------------------------------------- configs
+def test_config1_curve_and_fd():
+    c = wl.config1()
+    g = c.grad_out()
+    ctrl, U, u, gout = T(c.ctrl), T(c.U), T(c.u), T(g)
+    gU = torch.full_like(U, 1.0)
+    out = nb.curve_fwd(ctrl, U, u, c.p).cpu().numpy()
+    grad = nb.curve_bwd(ctrl, U, u, gout, c.p, grad_U=gU).cpu().numpy()
+    assert torch.all(gU == 0)
+    ref = oracle.curve_fwd(c.ctrl, c.U, c.u, c.p)
+    refg = oracle.curve_bwd(c.ctrl, c.U, c.u, g, c.p)
+    assert fwd_err(out, ref, c.ctrl) <= FWD_TOL
+    assert bwd_err(grad, refg) <= BWD_TOL
+    # config 1 asks for fwd+bwd vs finite differences: central FD of the fp64 oracle
+    fd = np.zeros_like(refg)
+    h = 1e-6
+    base = c.ctrl.astype(np.float64)
+    for idx in np.ndindex(base.shape):
+        cp, cm = base.copy(), base.copy()
+        cp[idx] += h
+        cm[idx] -= h
+        fd[idx] = (np.sum(oracle.curve_fwd(cp, c.U, c.u, c.p) * g) - np.sum(oracle.curve_fwd(cm, c.U, c.u, c.p) * g)) / (2 * h)
+    assert bwd_err(grad, fd) <= BWD_TOL
+
+
+@pytest.mark.parametrize("tables", [False, True])
+def test_config2(tables):
+    check_surface(wl.config2(), tables=tables)
+
+
+def test_config3():
+    check_surface(wl.config3())
+
+
+def test_config4_small_batch():
+    check_surface(wl.config4(B=48))
+
+
+def test_config4_batched_knots():
+    check_surface(wl.config4(B=24, knots_batched=True))
+
+
+def test_config5_shape_reduced_grid():
+    """256x256 net on a 1024x1024 grid: many row blocks and column blocks -> workspace + reduce."""
+    w = wl.config5(n_u=1024, n_v=1024)
+    sh = _abi.nurbs_shape(1, 256, 256, 3, 3, 1024, 1024, 0)
+    assert nb.bwd_workspace_bytes(sh) > 0
+    check_surface(w)
+
+
+# --------------------------------------------------------------------------- degrees / shapes
+@pytest.mark.parametrize("p,q", [(1, 1), (1, 5), (2, 3), (3, 2), (4, 4), (5, 1), (5, 5)])
+def test_degrees(p, q):
+    rng_seed = 10 * p + q
+    w = wl.surfaces(f"deg{p}{q}", B=3, n=p + 9, m=q + 6, p=p, q=q, n_u=70, n_v=131, seed=rng_seed, knots_batched=(p % 2 == 1))
+    check_surface(w, tables=False)
+
+
+@pytest.mark.parametrize("n_v", [1, 3, 130, 257, 300])
+def test_ragged_columns_and_non_tma_path(n_v):
+    """n_v not a multiple of 4 takes the non-TMA path; n_v > 128 has ragged column blocks."""
+    w = wl.surfaces("ragged", B=2, n=11, m=9, p=3, q=3, n_u=45, n_v=n_v, seed=n_v)
+    check_surface(w)
+
+
+@pytest.mark.parametrize("force_no_tma", [False, True])
+def test_tma_and_direct_paths_agree(force_no_tma, monkeypatch):
+    w = wl.config4(B=8)
+    g = w.grad_out(1)
+    a = run_surface(w, g)
+    monkeypatch.setenv("NURBS_NO_TMA", "1")
+    b = run_surface(w, g)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_sparse_samples_dense_knots():
+    """Fewer samples than spans: the row window jumps by more than p+1 rows."""
+    w = wl.surfaces("sparse", B=2, n=60, m=40, p=3, q=2, n_u=7, n_v=5, seed=3)
+    check_surface(w)
+
+
+# --------------------------------------------------------------------------- adversarial
+def adversarial_surface(seed, p=3, q=3, n=12, m=10, mult=None, wlo=0.05, whi=20.0):
+    rng = np.random.default_rng(seed)
+    def knots(n, p):
+        inner = np.sort(rng.uniform(0.05, 0.95, n - p - 1)).astype(np.float32)
+        if mult and len(inner) > mult:
+            inner[1:1 + mult] = inner[1]          # an interior knot of multiplicity `mult`
+        return np.concatenate([np.zeros(p + 1, np.float32), np.sort(inner), np.ones(p + 1, np.float32)])
+    U, V = knots(n, p), knots(m, q)
+    # samples: every knot, its fp32 neighbours, 0 and 1, plus random
+    def samples(K):
+        s = set(K.tolist())
+        for k in K:
+            s.add(float(np.nextafter(np.float32(k), np.float32(2))))
+            s.add(float(np.nextafter(np.float32(k), np.float32(-1))))
+        s |= set(rng.uniform(0, 1, 40).astype(np.float32).tolist())
+        return np.array(sorted(x for x in s if 0.0 <= x <= 1.0), dtype=np.float32)
+    ctrl = wl.random_net(rng, (2, n, m), wlo, whi)
+    return wl.Surfaces("adv", p, q, ctrl, U, V, samples(U), samples(V))
+
+
+@pytest.mark.parametrize("seed,mult", [(0, None), (1, 2), (2, 3)])
+def test_adversarial_knots_and_weights(seed, mult):
+    w = adversarial_surface(seed, mult=mult)
+    check_surface(w, tables=bool(seed % 2))
+
+
+def test_spans_bit_exact_in_tables():
+    for w in [wl.config2(), wl.config3(), adversarial_surface(5, mult=3), wl.config5(n_u=8192, n_v=64)]:
+        sh = _abi.nurbs_shape(w.B, w.n, w.m, w.p, w.q, w.n_u, w.n_v, 0)
+        U, V, u, v = T(w.U), T(w.V), T(w.u), T(w.v)
+        tab = nb.Tables.build(sh, U, V, u, v)
+        torch.cuda.synchronize()
+        buf = tab.buf.cpu().numpy()
+        hdr = buf[:64].view(np.int32)
+        assert hdr[0] == 0x4E524253
+        np_r = hdr[5]
+        off = 256
+        span_u = buf[off:off + 4 * w.n_u].view(np.int32)
+        su, Nu = oracle.spans(w.n, w.p, w.U, w.u)
+        np.testing.assert_array_equal(span_u, su)
+        off = (off + 4 * w.n_u + 255) // 256 * 256
+        Nu_gpu = buf[off:off + 4 * w.n_u * np_r].view(np.float32).reshape(w.n_u, np_r)[:, :w.p + 1]
+        assert np.max(np.abs(Nu_gpu - Nu)) <= 2e-6
+        off = (off + 4 * w.n_u * np_r + 255) // 256 * 256
+        sv, _ = oracle.spans(w.m, w.q, w.V, w.v)
+        np.testing.assert_array_equal(buf[off:off + 4 * w.n_v].view(np.int32), sv)
+
+
+def test_config1_hits_interior_knots_exactly():
+    c = wl.config1()
+    sh = _abi.nurbs_shape(1, c.n, 1, c.p, 0, c.n_u, 1, 0)
+    tab = nb.Tables.build(sh, T(c.U), None, T(c.u), None)
+    torch.cuda.synchronize()
+    buf = tab.buf.cpu().numpy()
+    hdr = buf[:64].view(np.int32)
+    # curve tables: the row part is empty, the columns are the curve (header is 256 bytes)
+    off = 256
+    span = buf[off:off + 4 * c.n_u].view(np.int32)
+    su, _ = oracle.spans(c.n, c.p, c.U, c.u)
+    np.testing.assert_array_equal(span, su)
+    assert span[33] == 4 and span[66] == 5 and hdr[8] == c.n_u
+
+
+# --------------------------------------------------------------------------- exactness pins on GPU
+def test_quarter_circle_radius_fp32():
+    s2 = np.float32(np.sqrt(2.0) / 2.0)
+    ctrl = np.array([[[1, 0, 0, 1], [1, 1, 0, s2], [0, 1, 0, 1]]], dtype=np.float32)
+    U = np.array([0, 0, 0, 1, 1, 1], dtype=np.float32)
+    u = wl.uniform_grid(1000)
+    out = nb.curve_fwd(T(ctrl), T(U), T(u), 2).cpu().numpy()
+    r = np.hypot(out[0, :, 0].astype(np.float64), out[0, :, 1].astype(np.float64))
+    assert np.max(np.abs(r - 1.0)) <= 1e-6
+
+
+def test_determinism_bitwise():
+    for w in [wl.config4(B=16), wl.config5(n_u=512, n_v=512)]:
+        g = w.grad_out(3)
+        a = run_surface(w, g)
+        b = run_surface(w, g)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+
+
+# --------------------------------------------------------------------------- edge cases
+def test_empty_inputs():
+    w = wl.surfaces("e", B=2, n=6, m=6, p=3, q=3, n_u=5, n_v=5, seed=1)
+    ctrl, U, V = T(w.ctrl), T(w.U), T(w.V)
+    u0 = torch.empty(0, device=DEV)
+    v = T(w.v)
+    out = nb.surface_fwd(ctrl, U, V, u0, v, 3, 3)
+    assert out.shape == (2, 0, 5, 3)
+    grad = nb.surface_bwd(ctrl, U, V, u0, v, torch.empty(2, 0, 5, 3, device=DEV), 3, 3,
+                          grad_ctrl=torch.full_like(ctrl, 5.0))
+    torch.cuda.synchronize()
+    assert torch.all(grad == 0)
+    out = nb.surface_fwd(ctrl[:0], U, V, T(w.u), v, 3, 3)
+    assert out.shape[0] == 0
+
+
+def test_single_sample_and_corner_interpolation():
+    w = wl.surfaces("one", B=3, n=5, m=7, p=2, q=3, n_u=1, n_v=1, seed=2)
+    out, grad = run_surface(w, w.grad_out(0))
+    np.testing.assert_allclose(out[:, 0, 0], w.ctrl[:, 0, 0, :3], rtol=0, atol=1e-6)   # S(0,0) = P_00
+    check_surface(w)
+
+
+def test_errors_and_checked_mode():
+    w = wl.surfaces("err", B=1, n=8, m=8, p=3, q=3, n_u=16, n_v=16, seed=4)
+    ctrl, U, V, u, v = T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v)
+    sh = nb.surface_shape(ctrl, U, u, v, 3, 3)
+    nb.nurbs_validate(sh, ctrl, U, V, u, v)
+    bad = U.clone(); bad[5], bad[6] = 0.9, 0.1
+    with pytest.raises(nb.NurbsError) as e:
+        nb.nurbs_validate(sh, ctrl, bad, V, u, v)
+    assert e.value.status == 3
+    with pytest.raises(nb.NurbsError) as e:
+        nb.nurbs_validate(sh, ctrl, U, V, u.flip(0).contiguous(), v)
+    assert e.value.status == 6
+    with pytest.raises(nb.NurbsError) as e:
+        nb.nurbs_validate(sh, ctrl, U, V, u - 0.5, v)
+    assert e.value.status in (4, 6)
+    neg = ctrl.clone(); neg[0, 2, 3, 3] = -1.0
+    with pytest.raises(nb.NurbsError) as e:
+        nb.nurbs_validate(sh, neg, U, V, u, v)
+    assert e.value.status == 5
+    with pytest.raises(nb.NurbsError) as e:
+        nb.Tables.build(sh, bad, V, u, v)
+    assert e.value.status == 3
+    big = wl.config5(n_u=256, n_v=256)
+    c5 = T(big.ctrl)
+    sh5 = nb.surface_shape(c5, T(big.U), T(big.u), T(big.v), 3, 3)
+    ws = nb.bwd_workspace_bytes(sh5)
+    with pytest.raises(nb.NurbsError) as e:
+        nb.nurbs_surface_bwd(sh5, c5, T(big.U), T(big.V), T(big.u), T(big.v), None,
+                             torch.zeros(1, 256, 256, 3, device=DEV), torch.empty_like(c5), None, None,
+                             torch.empty(16, dtype=torch.uint8, device=DEV), 16)
+    assert e.value.status == 8 and ws > 16
+
+
+# --------------------------------------------------------------------------- full BASELINE sizes
+def test_config4_full_size_sampled():
+    """The bench workload (B=4096, 16x16, 128^2) in the bench launch configuration; surfaces
+    are independent, so the oracle checks a sample of whole surfaces."""
+    w = wl.config4()
+    g = w.grad_out(4)
+    out, grad = run_surface(w, g, tables=True)
+    for k in [0, 1, 777, 2048, 4095]:
+        sub = wl.Surfaces("s", w.p, w.q, w.ctrl[k:k + 1], w.U, w.V, w.u, w.v)
+        ro = oracle.surface_fwd(sub.ctrl, w.U, w.V, w.u, w.v, w.p, w.q)
+        rg = oracle.surface_bwd(sub.ctrl, w.U, w.V, w.u, w.v, g[k:k + 1], w.p, w.q)
+        assert fwd_err(out[k:k + 1], ro, sub.ctrl) <= FWD_TOL
+        assert bwd_err(grad[k:k + 1], rg) <= BWD_TOL
+    # a property at any size: translation invariance sum_ij dP_ij = sum_pts g (per surface)
+    lhs = grad[..., :3].astype(np.float64).sum(axis=(1, 2))
+    rhs = g.astype(np.float64).sum(axis=(1, 2))
+    scale = np.abs(g).astype(np.float64).sum(axis=(1, 2))
+    assert np.max(np.abs(lhs - rhs) / scale) <= 1e-5
+
+
+def test_config5_full_size_sampled():
+    """One 256x256 net on the 8192^2 grid: sampled output rows and sampled control points."""
+    w = wl.config5()
+    g = w.grad_out(5)
+    out, grad = run_surface(w, g, tables=True)
+    rows = [0, 1, 4095, 8190, 8191]
+    ro = oracle.surface_fwd(w.ctrl, w.U, w.V, w.u[rows], w.v, w.p, w.q)
+    assert fwd_err(out[:, rows], ro, w.ctrl) <= FWD_TOL
+    sel = [(0, i, j) for i in (0, 1, 77, 128, 254, 255) for j in (0, 3, 100, 200, 255)]
+    rg = oracle.surface_bwd_selected(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q, sel)
+    got = np.array([grad[k, i, j] for (k, i, j) in sel])
+    # normwise: divide by max|d| over the whole tensor (dP and dw separately)
+    assert np.max(np.abs(got[:, :3] - rg[:, :3])) / np.max(np.abs(grad[..., :3])) <= BWD_TOL
+    assert np.max(np.abs(got[:, 3] - rg[:, 3])) / np.max(np.abs(grad[..., 3])) <= BWD_TOL
+    lhs = grad[0, ..., :3].astype(np.float64).sum(axis=(0, 1))
+    rhs = g[0].astype(np.float64).sum(axis=(0, 1))
+    assert np.max(np.abs(lhs - rhs)) / np.abs(g).astype(np.float64).sum() <= 1e-5
