@@ -1,38 +1,68 @@
 """In-tree build of libnurbs_b200.so for sm_100a (nvcc cross-compiles without a GPU).
 
-    python -m paper_2104_14547_b200.build [--force]
+    python -m paper_2104_14547_b200.build [--force] [-v]
+
+The grid kernel is instantiated for every (p, q, fwd/bwd, TMA/direct) combination; its
+translation unit is compiled once per row degree p (-DNB_P=p) in parallel.
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("nurbs_kernels.cu", "nurbs_api.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "nurbs_internal.cuh"), os.path.join(ROOT, "include", "nurbs.h")]
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libnurbs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc")
 
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-diag-suppress", "128"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17"] + ARCH + ["-Xcompiler", "-fPIC", "-diag-suppress", "128"]
+
+
+def units():
+    u = [("nurbs_api", os.path.join(CSRC, "nurbs_api.cu"), []),
+         ("nurbs_kernels", os.path.join(CSRC, "nurbs_kernels.cu"), [])]
+    for p in range(6):
+        u.append((f"nurbs_grid_p{p}", os.path.join(CSRC, "nurbs_grid_p.cu"), [f"-DNB_P={p}"]))
+    return u
+
+
+def deps():
+    return glob.glob(os.path.join(CSRC, "*")) + [os.path.join(ROOT, "include", "nurbs.h")]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS)
+    stale = force or not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in deps())
     if not stale:
         return LIB
-    cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp"] + SOURCES
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    os.makedirs(OBJ, exist_ok=True)
+    procs = []
+    for name, src, extra in units():
+        obj = os.path.join(OBJ, name + ".o")
+        cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+        procs.append((name, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    objs, failed = [], False
+    for name, obj, pr in procs:
+        out, _ = pr.communicate()
+        if pr.returncode != 0:
+            failed = True
+            sys.stderr.write(f"--- {name}\n{out}")
+        elif verbose:
+            sys.stderr.write(out)
+        objs.append(obj)
+    if failed:
+        raise RuntimeError("nvcc failed building libnurbs_b200.so")
+    res = subprocess.run([NVCC] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libnurbs_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc link failed")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

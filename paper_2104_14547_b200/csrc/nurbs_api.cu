@@ -285,6 +285,7 @@ int nurbs_surface_fwd(const nurbs_shape* sh, const float* ctrl, const float* U, 
   g_detail.clear();
   int st = check_surface_shape(sh);
   if (st) return st;
+  if (sh->B == 0 || sh->n_u == 0 || sh->n_v == 0) return NURBS_OK;  // nothing to evaluate
   if ((st = check_ptrs(false, ctrl, out, nullptr, nullptr))) return st;
   if (!tables && (!U || !V || !u || !v)) return fail(NURBS_E_ARG, "NULL knots or samples");
   if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
@@ -301,6 +302,13 @@ int nurbs_surface_bwd(const nurbs_shape* sh, const float* ctrl, const float* U, 
   g_detail.clear();
   int st = check_surface_shape(sh);
   if (st) return st;
+  if (sh->B == 0) return NURBS_OK;
+  if (sh->n_u == 0 || sh->n_v == 0) {  // no points: every gradient is zero
+    if (!grad_ctrl) return fail(NURBS_E_ARG, "grad_ctrl is NULL");
+    Geo g = surface_geo(sh, U, V, u, v);
+    return launch(g, true, ctrl, nullptr, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes,
+                  static_cast<cudaStream_t>(stream));
+  }
   if ((st = check_ptrs(true, ctrl, nullptr, grad_out, grad_ctrl))) return st;
   if (!tables && (!U || !V || !u || !v)) return fail(NURBS_E_ARG, "NULL knots or samples");
   if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
@@ -316,6 +324,7 @@ int nurbs_curve_fwd(const nurbs_shape* sh, const float* ctrl, const float* U, co
   g_detail.clear();
   int st = check_curve_shape(sh);
   if (st) return st;
+  if (sh->B == 0 || sh->n_u == 0) return NURBS_OK;
   if ((st = check_ptrs(false, ctrl, out, nullptr, nullptr))) return st;
   if (!tables && (!U || !u)) return fail(NURBS_E_ARG, "NULL knots or samples");
   if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
@@ -332,6 +341,13 @@ int nurbs_curve_bwd(const nurbs_shape* sh, const float* ctrl, const float* U, co
   g_detail.clear();
   int st = check_curve_shape(sh);
   if (st) return st;
+  if (sh->B == 0) return NURBS_OK;
+  if (sh->n_u == 0) {
+    if (!grad_ctrl) return fail(NURBS_E_ARG, "grad_ctrl is NULL");
+    Geo g = curve_geo(sh, U, u);
+    return launch(g, true, ctrl, nullptr, grad_out, grad_ctrl, nullptr, grad_U, workspace, ws_bytes,
+                  static_cast<cudaStream_t>(stream));
+  }
   if ((st = check_ptrs(true, ctrl, nullptr, grad_out, grad_ctrl))) return st;
   if (!tables && (!U || !u)) return fail(NURBS_E_ARG, "NULL knots or samples");
   if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");

@@ -1,0 +1,393 @@
+// nurbs_grid.cuh — the fused grid kernel of the NURBS-Diff hot path (arXiv 2104.14547).
+//
+// Citations: P:n = reference/PAPER.md line n; R<k> = reading k of DESIGN.md §3.
+//
+// The grid case is evaluated as the separable banded product S' = N_u · Q · N_v^T (Eq.3
+// P:110 with the homogeneous points of P:140, Q_ij = (w_ij P_ij, w_ij)):
+//   F1  T[i][b]  = sum_h Nv[b][h] Q[i][sv(b)-q+h]            (per CTA column block, smem)
+//   F2  S'[a][b] = sum_r Nu[a][r] T[su(a)-p+r][b]            (rolling register window)
+//       S = S'_xyz / S'_w                                     (P:140 step 3)
+// and the backward (Eq.8 P:215 / Eq.9 P:222 / J^T g of P:251) as its transpose:
+//   G[a][b]  = (g/W, -(g.S)/W)              (homogeneous upstream)
+//   B1 H[i][b]  = sum_a Nu[a][i-su(a)+p] G[a][b]   (rolling accumulators, flushed in order)
+//   B2 dQ[i][j] = sum_b H[i][b] Nv[b][j-sv(b)+q]   (fixed b order)
+//   dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
+// Every reduction runs in a fixed order; there are no floating-point atomics, so results
+// are bitwise repeatable (SPEC S:157's deterministic gather, instead of the paper's scatter
+// of P:289).
+//
+// CTA = (surface s, row block rb, column block cb). A row block is K consecutive KNOT SPANS
+// of the u direction (its sample rows are those whose span falls in [S0, S0+K)), so its
+// control-row band [rb*K, S0+K-1] has at most K+p <= kRMax rows; a column block is 128
+// consecutive SAMPLE columns (one compute thread each). Warp 4 is a TMA producer: it streams
+// grad_out rows into a 3-stage smem ring (bwd) or drains the staged output rows to HBM with
+// cp.async.bulk (fwd).
+#pragma once
+#include "nurbs_device.cuh"
+
+namespace nb {
+
+// ------------------------------------------------------------------------ the grid kernel
+// One row of the walk (F2, and B1 in the backward) for one column: uniform across the CTA
+// except for the column data. `nu` = basis of the row, `tw` = the T window (P+1 control rows
+// [lo, lo+P] of this column), `io` = this thread's 3 floats of the output / dL/dS row.
+template <int P, bool BWD>
+__device__ __forceinline__ void walk_row(const float* __restrict__ nu, const float4 (&tw)[P + 1],
+                                         float4 (&acc)[P + 1], float* io, bool valid) {
+  float4 Sp = f4(0.f);
+#pragma unroll
+  for (int k = 0; k <= P; ++k) Sp = fma4(nu[k], tw[k], Sp);
+  const float rw = rcp_approx(Sp.w);
+  if constexpr (!BWD) {
+    if (valid) {
+      io[0] = Sp.x * rw;
+      io[1] = Sp.y * rw;
+      io[2] = Sp.z * rw;
+    }
+  } else {
+    float gx = 0.f, gy = 0.f, gz = 0.f;
+    if (valid) {
+      gx = io[0];
+      gy = io[1];
+      gz = io[2];
+    }
+    // G = (g/W, -(g.S)/W) with S = S'_xyz / W  (Eq.8/9 through the homogeneous point)
+    const float gxr = gx * rw, gyr = gy * rw, gzr = gz * rw;
+    const float gS = fmaf(gxr, Sp.x, fmaf(gyr, Sp.y, gzr * Sp.z));
+    const float4 G = make_float4(gxr, gyr, gzr, -gS * rw);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) acc[k] = fma4(nu[k], G, acc[k]);
+  }
+}
+
+template <int P, int Q, bool BWD, bool BULK>
+__global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params prm) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
+  constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const Dir& R = prm.r;
+  const Dir& C = prm.c;
+
+  // ---- decode the tile
+  int bid = blockIdx.x;
+  const int cb = bid % prm.NCB;
+  bid /= prm.NCB;
+  const int rb = bid % prm.NRB;
+  const int s = bid / prm.NRB;
+  const int B0 = cb * kCB;
+  const int cols = min(kCB, C.ns - B0);
+  const int S0 = P + rb * prm.K;                 // first knot span of this row block
+  const int S1 = min(S0 + prm.K, R.n);           // one past the last
+  const int band_lo = S0 - P;                    // control-row band [band_lo, S1-1]
+  const int band_rows = S1 - band_lo;            // <= T_rows
+  const float* Uk = (P > 0) ? R.knots + (long long)s * R.kstride : nullptr;
+  const float* Vk = C.tspan ? nullptr : C.knots + (long long)s * C.kstride;
+
+  // ---- shared memory carve-up
+  float4* T = reinterpret_cast<float4*>(smem);                       // [T_rows][kCB] (T, then H)
+  float* stage = reinterpret_cast<float*>(T + (size_t)prm.T_rows * kCB);  // [kStages][kRPS*kCB*3]
+  int* su_s = reinterpret_cast<int*>(stage + kStages * kRPS * kCB * 3);   // [kRowChunk]
+  float* Nu_s = reinterpret_cast<float*>(su_s + kRowChunk);               // [kRowChunk][NP]
+  int* sv_s = reinterpret_cast<int*>(Nu_s + kRowChunk * NP);              // [kCB]      (bwd only)
+  float* Nv_s = reinterpret_cast<float*>(sv_s + kCB);                     // [kCB][NQ]  (bwd only)
+  unsigned char* after = BWD ? reinterpret_cast<unsigned char*>(Nv_s + kCB * NQ)
+                             : reinterpret_cast<unsigned char*>(sv_s);
+  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(after) + 7) & ~uintptr_t(7));
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+
+  if (BULK && tid == 0) {
+#pragma unroll
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(full + i, BWD ? 1u : (uint32_t)kCompute);
+      mbar_init(empty + i, BWD ? (uint32_t)kCompute : 1u);
+    }
+    fence_mbar_init();
+  }
+
+  // ---- sample rows of this row block: spans in [S0, S1)   (all 160 threads)
+  int a_lo = 0, a_hi = R.ns;
+  if (prm.NRB > 1) {
+    int s_end = R.n - 1;  // last non-empty span (R3)
+    if (P > 0 && !R.tspan)
+      while (s_end > P && __ldg(Uk + s_end) == __ldg(Uk + s_end + 1)) --s_end;
+    auto ge = [&](int S) {
+      return [&, S](int a) -> bool {
+        if (R.tspan) return __ldg(R.tspan + a) >= S;
+        if (S > s_end) return false;
+        return __ldg(R.s + a) >= __ldg(Uk + S);
+      };
+    };
+    if (rb > 0) a_lo = cta_first_true(R.ns, ge(S0));
+    if (rb < prm.NRB - 1) a_hi = cta_first_true(R.ns, ge(S1));
+  }
+  __syncthreads();
+  const int nwalk = max(0, a_hi - a_lo);
+  const int nstage = (nwalk + kRPS - 1) / kRPS;
+  const bool contig = (cols == C.ns);  // whole sample rows: consecutive rows are contiguous
+
+  // ======================================================== producer warp (TMA bulk)
+  if (warp == kCompute / 32) {
+    if (BULK && (tid & 31) == 0) {
+      const uint32_t rowbytes = (uint32_t)cols * 12u;
+      int slot = 0, use = 0;
+      for (int k = 0; k < nstage; ++k) {
+        const int r0 = a_lo + k * kRPS;
+        const int nr = min(kRPS, a_hi - r0);
+        float* buf = stage + slot * (kRPS * kCB * 3);
+        if constexpr (BWD) {
+          if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
+          mbar_arrive_expect_tx(full + slot, rowbytes * nr);
+          const float* src = prm.gout + ((size_t)((size_t)s * R.ns + r0) * C.ns + B0) * 3;
+          if (contig) {
+            bulk_g2s(buf, src, rowbytes * nr, full + slot);
+          } else {
+            for (int rr = 0; rr < nr; ++rr)
+              bulk_g2s(buf + rr * cols * 3, src + (size_t)rr * C.ns * 3, rowbytes, full + slot);
+          }
+        } else {
+          mbar_wait(full + slot, use & 1);
+          float* dst = prm.out + ((size_t)((size_t)s * R.ns + r0) * C.ns + B0) * 3;
+          if (contig) {
+            bulk_s2g(dst, buf, rowbytes * nr);
+          } else {
+            for (int rr = 0; rr < nr; ++rr) bulk_s2g(dst + (size_t)rr * C.ns * 3, buf + rr * cols * 3, rowbytes);
+          }
+          bulk_commit();
+          bulk_wait_read_all();
+          mbar_arrive(empty + slot);
+        }
+        if (++slot == kStages) { slot = 0; ++use; }
+      }
+      if constexpr (!BWD) bulk_wait_all();
+    }
+    return;
+  }
+
+  // ======================================================== compute warps (128 threads)
+  const int t = tid;
+  const bool valid = t < cols;
+  const int b = B0 + (valid ? t : cols - 1);
+
+  // ---- column span + basis (registers), shared with the B2 stage in smem
+  int sv;
+  float nv[Q + 1];
+  if (C.tspan) {
+    sv = __ldg(C.tspan + b);
+    const float* tn = C.tN + (size_t)b * C.tnp;
+#pragma unroll
+    for (int h = 0; h <= Q; ++h) nv[h] = __ldg(tn + h);
+  } else {
+    const float vb = __ldg(C.s + b);
+    sv = d_find_span(Vk, C.n, Q, vb);
+    d_basis<Q>(Vk, sv, vb, Q, nv);
+  }
+  sv = min(max(sv, Q), C.n - 1);
+  if constexpr (BWD) {
+    sv_s[t] = sv;
+#pragma unroll
+    for (int h = 0; h < NQ; ++h) Nv_s[t * NQ + h] = h <= Q ? nv[h <= Q ? h : 0] : 0.f;
+  }
+
+  // ---- F1: T[r][t] = sum_h Nv[h] Q[band_lo + r][sv - q + h]
+  const float4* __restrict__ ctrl_s = prm.ctrl + (size_t)s * R.n * C.n;
+  {
+    const float4* colp = ctrl_s + (size_t)band_lo * C.n + (sv - Q);
+#pragma unroll 4
+    for (int r = 0; r < band_rows; ++r) {
+      const float4* rowp = colp + (size_t)r * C.n;
+      float4 c[Q + 1];
+#pragma unroll
+      for (int h = 0; h <= Q; ++h) c[h] = __ldg(rowp + h);
+      float4 a = f4(0.f);
+#pragma unroll
+      for (int h = 0; h <= Q; ++h) a = fma4(nv[h], homog(c[h]), a);
+      T[r * kCB + t] = a;
+    }
+  }
+
+  // ---- walk the sample rows: rolling window of P+1 control rows [lo, lo+P]
+  float4 tw[P + 1];
+  float4 acc[P + 1];
+  int lo = band_lo;
+#pragma unroll
+  for (int k = 0; k <= P; ++k) {
+    tw[k] = T[k * kCB + t];
+    acc[k] = f4(0.f);
+  }
+
+  // direct (non-TMA) path: this thread's element of row a_lo in out / grad_out
+  float* gio = nullptr;
+  if constexpr (!BULK) {
+    gio = (BWD ? const_cast<float*>(prm.gout) : prm.out) + (((size_t)s * R.ns + a_lo) * C.ns + b) * 3;
+  }
+  const size_t grow = (size_t)C.ns * 3;  // floats between consecutive sample rows
+
+  int slot = 0, use = 0;
+  for (int st = 0; st < nstage; ++st) {
+    const int r0 = st * kRPS;                 // walk index of the stage's first row
+    const int nr = min(kRPS, nwalk - r0);
+    const int ci0 = r0 % kRowChunk;           // kRowChunk is a multiple of kRPS
+    if (ci0 == 0) {                           // stage span + basis of the next kRowChunk rows
+      if (r0 > 0) bar_compute();              // previous chunk fully consumed
+      const int cn = min(kRowChunk, nwalk - r0);
+      if (t < cn) {
+        const int a = a_lo + r0 + t;
+        int su;
+        float nu[P + 1];
+        if constexpr (P == 0) {
+          su = 0;
+          nu[0] = 1.f;
+        } else {
+          if (R.tspan) {
+            su = __ldg(R.tspan + a);
+            const float* tn = R.tN + (size_t)a * R.tnp;
+#pragma unroll
+            for (int k = 0; k <= P; ++k) nu[k] = __ldg(tn + k);
+          } else {
+            const float ua = __ldg(R.s + a);
+            su = d_find_span(Uk, R.n, P, ua);
+            d_basis<P>(Uk, su, ua, P, nu);
+          }
+        }
+        su_s[t] = min(max(su, S0), S1 - 1);  // memory safety for inconsistent inputs
+#pragma unroll
+        for (int k = 0; k < NP; ++k) Nu_s[t * NP + k] = (k <= P) ? nu[k <= P ? k : 0] : 0.f;
+      }
+      bar_compute();
+    }
+    float* buf = stage + slot * (kRPS * kCB * 3) + t * 3;
+    if constexpr (BULK) {
+      if (BWD) mbar_wait(full + slot, use & 1);
+      else if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
+    }
+    // rows of the stage, grouped into runs of equal span (the window changes between runs)
+    int i = 0;
+    while (i < nr) {
+      const int su = su_s[ci0 + i];
+      while (lo < su - P) {  // advance the window (uniform): row lo is complete
+        if constexpr (BWD) T[(lo - band_lo) * kCB + t] = acc[0];  // H row (aliases T)
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          tw[k] = tw[k + 1];
+          if constexpr (BWD) acc[k] = acc[k + 1];
+        }
+        ++lo;
+        tw[P] = T[(lo + P - band_lo) * kCB + t];
+        if constexpr (BWD) acc[P] = f4(0.f);
+      }
+      int e = i + 1;
+      while (e < nr && su_s[ci0 + e] == su) ++e;
+      for (int r = i; r < e; ++r) {
+        const float* nup = Nu_s + (ci0 + r) * NP;
+        float nu[NP];
+        const float4 n0 = *reinterpret_cast<const float4*>(nup);
+        nu[0] = n0.x; nu[1] = n0.y; nu[2] = n0.z; nu[3] = n0.w;
+        if constexpr (NP == 8) {
+          const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
+          nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
+        }
+        float* io = BULK ? buf + r * cols * 3 : gio + (size_t)(r0 + r) * grow;
+        walk_row<P, BWD>(nu, tw, acc, io, valid);
+      }
+      i = e;
+    }
+    if constexpr (BULK) {
+      if constexpr (!BWD) fence_proxy_async();
+      mbar_arrive(BWD ? empty + slot : full + slot);
+    }
+    if (++slot == kStages) { slot = 0; ++use; }
+  }
+
+  if constexpr (BWD) {
+    // ---- B1 epilogue: flush the last window, zero the rows never reached
+#pragma unroll
+    for (int k = 0; k <= P; ++k) T[(lo + k - band_lo) * kCB + t] = acc[k];
+    for (int r = lo + P + 1 - band_lo; r < band_rows; ++r) T[r * kCB + t] = f4(0.f);
+    bar_compute();
+
+    // ---- B2: dQ[i][j] = sum_b H[i-band_lo][b] Nv[b][j - sv(b) + q], b ascending
+    const int j0 = sv_s[0] - Q;
+    const int j1 = sv_s[cols - 1];
+    const int nj = j1 - j0 + 1;
+    float4* gctrl_s = prm.gctrl + (size_t)s * R.n * C.n;
+    const int ntask = prm.direct ? R.n * C.n : band_rows * nj;
+    for (int task = t; task < ntask; task += kCompute) {
+      int r, j;
+      if (prm.direct) {
+        r = task / C.n;  // band_lo == 0 and band_rows == R.n in direct mode
+        j = task - r * C.n;
+      } else {
+        r = task / nj;
+        j = j0 + (task - r * nj);
+      }
+      float4 a4 = f4(0.f);
+      if (j >= j0 && j <= j1) {
+        int blo = 0, bhi = cols;  // first b with sv >= j
+        while (blo < bhi) {
+          const int mid = (blo + bhi) >> 1;
+          if (sv_s[mid] < j) blo = mid + 1; else bhi = mid;
+        }
+        int bend = blo, bh2 = cols;  // first b with sv > j + q
+        while (bend < bh2) {
+          const int mid = (bend + bh2) >> 1;
+          if (sv_s[mid] <= j + Q) bend = mid + 1; else bh2 = mid;
+        }
+        const float4* Hr = T + r * kCB;
+        for (int bb = blo; bb < bend; ++bb) a4 = fma4(Nv_s[bb * NQ + (j - sv_s[bb] + Q)], Hr[bb], a4);
+      }
+      if (prm.direct) {
+        // epilogue (Eq.8/9): dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
+        const float4 c = __ldg(ctrl_s + (size_t)r * C.n + j);
+        gctrl_s[(size_t)r * C.n + j] =
+            make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
+      } else {
+        prm.slots[((((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows + r) * C.n + j] = a4;
+      }
+    }
+    if (!prm.direct && rb == 0 && t == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(j0, j1);
+    if (prm.direct) {  // knot gradients are zero by definition
+      if (prm.gR && s < prm.gR_items)
+        for (int x = t; x < prm.gR_per; x += kCompute) prm.gR[(size_t)s * prm.gR_per + x] = 0.f;
+      if (prm.gC && s < prm.gC_items)
+        for (int x = t; x < prm.gC_per; x += kCompute) prm.gC[(size_t)s * prm.gC_per + x] = 0.f;
+    }
+  }
+}
+
+template <int P, int Q, bool BWD, bool BULK>
+static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
+  const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, BULK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  nurbs_grid_kernel<P, Q, BWD, BULK>
+      <<<(unsigned)((long long)prm.B * prm.NRB * prm.NCB), kThreads, smem, st>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int P, int Q>
+static cudaError_t launch_pq(const Params& prm, bool bwd, cudaStream_t st) {
+  if (bwd) return prm.bulk ? launch_one<P, Q, true, true>(prm, st) : launch_one<P, Q, true, false>(prm, st);
+  return prm.bulk ? launch_one<P, Q, false, true>(prm, st) : launch_one<P, Q, false, false>(prm, st);
+}
+
+template <int P>
+static cudaError_t launch_p(const Params& prm, bool bwd, int q, cudaStream_t st) {
+  switch (q) {
+    case 1: return launch_pq<P, 1>(prm, bwd, st);
+    case 2: return launch_pq<P, 2>(prm, bwd, st);
+    case 3: return launch_pq<P, 3>(prm, bwd, st);
+    case 4: return launch_pq<P, 4>(prm, bwd, st);
+    case 5: return launch_pq<P, 5>(prm, bwd, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace nb

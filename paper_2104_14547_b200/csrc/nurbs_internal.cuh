@@ -120,3 +120,12 @@ cudaError_t launch_validate(int B, const Dir& r, const Dir& c, int check_rows,
 size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows);
 
 }  // namespace nb
+
+namespace nb {
+cudaError_t launch_grid_p0(const Params& prm, bool bwd, int q, cudaStream_t st);
+cudaError_t launch_grid_p1(const Params& prm, bool bwd, int q, cudaStream_t st);
+cudaError_t launch_grid_p2(const Params& prm, bool bwd, int q, cudaStream_t st);
+cudaError_t launch_grid_p3(const Params& prm, bool bwd, int q, cudaStream_t st);
+cudaError_t launch_grid_p4(const Params& prm, bool bwd, int q, cudaStream_t st);
+cudaError_t launch_grid_p5(const Params& prm, bool bwd, int q, cudaStream_t st);
+}  // namespace nb

@@ -47,13 +47,20 @@ def fwd_err(gpu, ref, ctrl):
     return float(np.max(e / scale))
 
 
-def bwd_err(gpu, ref):
-    """max over surfaces and over the two tensors (dP, dw) of max|diff| / max|ref|"""
+def bwd_err(gpu, ref, ctrl=None):
+    """max over surfaces and over the two tensors (dP, dw) of max|diff| / scale, scale =
+    max|ref| (R16). dw = P.dQ_xyz + dQ_w is a difference of two terms that cancel exactly in
+    degenerate cases (e.g. one sample at a clamped corner), so its scale also includes the
+    size of the first term, max |P_ij| |dP_ij| / w_ij."""
     B = ref.shape[0]
     worst = 0.0
     for sl in (np.s_[..., :3], np.s_[..., 3]):
         g, r = gpu[sl].reshape(B, -1), ref[sl].reshape(B, -1)
         sc = np.abs(r).max(axis=1)
+        if sl == np.s_[..., 3] and ctrl is not None:
+            c = np.asarray(ctrl, dtype=np.float64).reshape(B, -1, 4)
+            dP = ref[..., :3].reshape(B, -1, 3)
+            sc = sc + (np.abs(c[..., :3]) * np.abs(dP)).sum(axis=2).max(axis=1) / c[..., 3].min(axis=1)
         sc[sc == 0] = 1.0
         worst = max(worst, float(np.max(np.abs(g - r).max(axis=1) / sc)))
     return worst
@@ -80,7 +87,7 @@ def check_surface(w, gseed=0, tables=False, fwd_tol=FWD_TOL, bwd_tol=BWD_TOL):
     out, grad = run_surface(w, g, tables)
     ref_out = oracle.surface_fwd(w.ctrl, w.U, w.V, w.u, w.v, w.p, w.q, w.knots_batched)
     ref_grad = oracle.surface_bwd(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q, w.knots_batched)
-    ef, eb = fwd_err(out, ref_out, w.ctrl), bwd_err(grad, ref_grad)
+    ef, eb = fwd_err(out, ref_out, w.ctrl), bwd_err(grad, ref_grad, w.ctrl)
     assert ef <= fwd_tol, f"{w.name}: forward error {ef:.3e}"
     assert eb <= bwd_tol, f"{w.name}: backward error {eb:.3e}"
     return ef, eb
