@@ -39,18 +39,15 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
   for (int k = 0; k <= P; ++k) Sp = fma4(nu[k], tw[k], Sp);
   const float rw = rcp_approx(Sp.w);
   if constexpr (!BWD) {
-    if (valid) {
+    if (valid) {  // always true in TMA staging (columns >= cols land in the unused row tail)
       io[0] = Sp.x * rw;
       io[1] = Sp.y * rw;
       io[2] = Sp.z * rw;
     }
   } else {
-    float gx = 0.f, gy = 0.f, gz = 0.f;
-    if (valid) {
-      gx = io[0];
-      gy = io[1];
-      gz = io[2];
-    }
+    const float gx = valid ? io[0] : 0.f;
+    const float gy = valid ? io[1] : 0.f;
+    const float gz = valid ? io[2] : 0.f;
     // G = (g/W, -(g.S)/W) with S = S'_xyz / W  (Eq.8/9 through the homogeneous point)
     const float gxr = gx * rw, gyr = gy * rw, gzr = gz * rw;
     const float gS = fmaf(gxr, Sp.x, fmaf(gyr, Sp.y, gzr * Sp.z));
@@ -129,9 +126,11 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   const bool contig = (cols == C.ns);  // whole sample rows: consecutive rows are contiguous
 
   // ======================================================== producer warp (TMA bulk)
+  // Stage slot = kRPS rows at a fixed smem row stride of kCB*3 floats.
   if (warp == kCompute / 32) {
     if (BULK && (tid & 31) == 0) {
       const uint32_t rowbytes = (uint32_t)cols * 12u;
+      const bool one_copy = contig && cols == kCB;  // the stage's rows are one contiguous span
       int slot = 0, use = 0;
       for (int k = 0; k < nstage; ++k) {
         const int r0 = a_lo + k * kRPS;
@@ -141,19 +140,19 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
           if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
           mbar_arrive_expect_tx(full + slot, rowbytes * nr);
           const float* src = prm.gout + ((size_t)((size_t)s * R.ns + r0) * C.ns + B0) * 3;
-          if (contig) {
+          if (one_copy) {
             bulk_g2s(buf, src, rowbytes * nr, full + slot);
           } else {
             for (int rr = 0; rr < nr; ++rr)
-              bulk_g2s(buf + rr * cols * 3, src + (size_t)rr * C.ns * 3, rowbytes, full + slot);
+              bulk_g2s(buf + rr * kCB * 3, src + (size_t)rr * C.ns * 3, rowbytes, full + slot);
           }
         } else {
           mbar_wait(full + slot, use & 1);
           float* dst = prm.out + ((size_t)((size_t)s * R.ns + r0) * C.ns + B0) * 3;
-          if (contig) {
+          if (one_copy) {
             bulk_s2g(dst, buf, rowbytes * nr);
           } else {
-            for (int rr = 0; rr < nr; ++rr) bulk_s2g(dst + (size_t)rr * C.ns * 3, buf + rr * cols * 3, rowbytes);
+            for (int rr = 0; rr < nr; ++rr) bulk_s2g(dst + (size_t)rr * C.ns * 3, buf + rr * kCB * 3, rowbytes);
           }
           bulk_commit();
           bulk_wait_read_all();
@@ -225,6 +224,34 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   }
   const size_t grow = (size_t)C.ns * 3;  // floats between consecutive sample rows
 
+  // One row of the walk: advance the window to the row's span if it changed (uniform across
+  // the CTA, rare: once per knot span), then F2 (+ B1). ci = row index in the smem tables.
+  auto row_step = [&](int ci, float* io) {
+    const int target = su_s[ci] - P;
+    if (target != lo) {
+      do {  // row lo is complete: in the backward it becomes H row lo (aliases T row lo)
+        if constexpr (BWD) T[(lo - band_lo) * kCB + t] = acc[0];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          tw[k] = tw[k + 1];
+          if constexpr (BWD) acc[k] = acc[k + 1];
+        }
+        ++lo;
+        tw[P] = T[(lo + P - band_lo) * kCB + t];
+        if constexpr (BWD) acc[P] = f4(0.f);
+      } while (lo < target);
+    }
+    const float* nup = Nu_s + ci * NP;
+    float nu[NP];
+    const float4 n0 = *reinterpret_cast<const float4*>(nup);
+    nu[0] = n0.x; nu[1] = n0.y; nu[2] = n0.z; nu[3] = n0.w;
+    if constexpr (NP == 8) {
+      const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
+      nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
+    }
+    walk_row<P, BWD>(nu, tw, acc, io, BULK && !BWD ? true : valid);
+  };
+
   int slot = 0, use = 0;
   for (int st = 0; st < nstage; ++st) {
     const int r0 = st * kRPS;                 // walk index of the stage's first row
@@ -258,45 +285,26 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
       }
       bar_compute();
     }
-    float* buf = stage + slot * (kRPS * kCB * 3) + t * 3;
     if constexpr (BULK) {
       if (BWD) mbar_wait(full + slot, use & 1);
       else if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
-    }
-    // rows of the stage, grouped into runs of equal span (the window changes between runs)
-    int i = 0;
-    while (i < nr) {
-      const int su = su_s[ci0 + i];
-      while (lo < su - P) {  // advance the window (uniform): row lo is complete
-        if constexpr (BWD) T[(lo - band_lo) * kCB + t] = acc[0];  // H row (aliases T)
+      float* buf = stage + slot * (kRPS * kCB * 3) + t * 3;
+      if (nr == kRPS) {
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-          tw[k] = tw[k + 1];
-          if constexpr (BWD) acc[k] = acc[k + 1];
-        }
-        ++lo;
-        tw[P] = T[(lo + P - band_lo) * kCB + t];
-        if constexpr (BWD) acc[P] = f4(0.f);
+        for (int r = 0; r < kRPS; ++r) row_step(ci0 + r, buf + r * kCB * 3);
+      } else {
+        for (int r = 0; r < nr; ++r) row_step(ci0 + r, buf + r * kCB * 3);
       }
-      int e = i + 1;
-      while (e < nr && su_s[ci0 + e] == su) ++e;
-      for (int r = i; r < e; ++r) {
-        const float* nup = Nu_s + (ci0 + r) * NP;
-        float nu[NP];
-        const float4 n0 = *reinterpret_cast<const float4*>(nup);
-        nu[0] = n0.x; nu[1] = n0.y; nu[2] = n0.z; nu[3] = n0.w;
-        if constexpr (NP == 8) {
-          const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
-          nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
-        }
-        float* io = BULK ? buf + r * cols * 3 : gio + (size_t)(r0 + r) * grow;
-        walk_row<P, BWD>(nu, tw, acc, io, valid);
-      }
-      i = e;
-    }
-    if constexpr (BULK) {
       if constexpr (!BWD) fence_proxy_async();
       mbar_arrive(BWD ? empty + slot : full + slot);
+    } else {
+      float* io = gio + (size_t)r0 * grow;
+      if (nr == kRPS) {
+#pragma unroll
+        for (int r = 0; r < kRPS; ++r) row_step(ci0 + r, io + r * grow);
+      } else {
+        for (int r = 0; r < nr; ++r) row_step(ci0 + r, io + r * grow);
+      }
     }
     if (++slot == kStages) { slot = 0; ++use; }
   }

@@ -14,8 +14,8 @@ namespace nb {
 constexpr int kCB = 128;          // sample columns per CTA block = compute threads
 constexpr int kCompute = 128;     // compute threads (4 warps)
 constexpr int kThreads = 160;     // + 1 producer warp issuing TMA bulk copies
-constexpr int kRPS = 4;           // sample rows per pipeline stage
-constexpr int kStages = 3;        // pipeline depth (stage ring)
+constexpr int kRPS = 8;           // sample rows per pipeline stage
+constexpr int kStages = 2;        // pipeline depth (stage ring)
 constexpr int kRowChunk = 64;     // rows whose span/basis are staged in smem at once
 constexpr int kMaxQ = 5;          // max column degree (runtime q)
 constexpr int kRMax = 16;         // max control rows in a row-block band (T/H smem rows)
