@@ -74,6 +74,37 @@ __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); 
 __device__ __forceinline__ float4 fma4(float s, float4 a, float4 acc) {
   return make_float4(fmaf(s, a.x, acc.x), fmaf(s, a.y, acc.y), fmaf(s, a.z, acc.z), fmaf(s, a.w, acc.w));
 }
+// Packed fp32x2 (sm_100 FFMA2 / FMUL2): a float4 is two 64-bit register pairs (x,y), (z,w);
+// a scalar factor is broadcast by ptxas into the .F32 operand form (no packing moves).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(a), "f"(b));
+  return d;
+}
+__device__ __forceinline__ float2 up2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// acc + s * a on float4 as two FFMA2 (same rounding as four fmaf).
+__device__ __forceinline__ float4 fma4v(float s, float4 a, float4 acc) {
+  const unsigned long long ss = pk2(s, s);
+  const float2 lo = up2(ffma2(ss, pk2(a.x, a.y), pk2(acc.x, acc.y)));
+  const float2 hi = up2(ffma2(ss, pk2(a.z, a.w), pk2(acc.z, acc.w)));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
 // homogeneous point P^w = (w x, w y, w z, w)   (P:140 step 3)
 __device__ __forceinline__ float4 homog(float4 c) { return make_float4(c.x * c.w, c.y * c.w, c.z * c.w, c.w); }
 

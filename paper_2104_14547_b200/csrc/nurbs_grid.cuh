@@ -36,12 +36,13 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
                                          float4 (&acc)[P + 1], float* io, bool valid) {
   float4 Sp = f4(0.f);
 #pragma unroll
-  for (int k = 0; k <= P; ++k) Sp = fma4(nu[k], tw[k], Sp);
+  for (int k = 0; k <= P; ++k) Sp = fma4v(nu[k], tw[k], Sp);
   const float rw = rcp_approx(Sp.w);
   if constexpr (!BWD) {
+    const float2 oxy = up2(fmul2(pk2(Sp.x, Sp.y), pk2(rw, rw)));
     if (valid) {  // always true in TMA staging (columns >= cols land in the unused row tail)
-      io[0] = Sp.x * rw;
-      io[1] = Sp.y * rw;
+      io[0] = oxy.x;
+      io[1] = oxy.y;
       io[2] = Sp.z * rw;
     }
   } else {
@@ -49,11 +50,12 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
     const float gy = valid ? io[1] : 0.f;
     const float gz = valid ? io[2] : 0.f;
     // G = (g/W, -(g.S)/W) with S = S'_xyz / W  (Eq.8/9 through the homogeneous point)
-    const float gxr = gx * rw, gyr = gy * rw, gzr = gz * rw;
-    const float gS = fmaf(gxr, Sp.x, fmaf(gyr, Sp.y, gzr * Sp.z));
-    const float4 G = make_float4(gxr, gyr, gzr, -gS * rw);
+    const float2 gxy = up2(fmul2(pk2(gx, gy), pk2(rw, rw)));
+    const float gzr = gz * rw;
+    const float gS = fmaf(gxy.x, Sp.x, fmaf(gxy.y, Sp.y, gzr * Sp.z));
+    const float4 G = make_float4(gxy.x, gxy.y, gzr, -gS * rw);
 #pragma unroll
-    for (int k = 0; k <= P; ++k) acc[k] = fma4(nu[k], G, acc[k]);
+    for (int k = 0; k <= P; ++k) acc[k] = fma4v(nu[k], G, acc[k]);
   }
 }
 
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
       for (int h = 0; h <= Q; ++h) c[h] = __ldg(rowp + h);
       float4 a = f4(0.f);
 #pragma unroll
-      for (int h = 0; h <= Q; ++h) a = fma4(nv[h], homog(c[h]), a);
+      for (int h = 0; h <= Q; ++h) a = fma4v(nv[h], homog(c[h]), a);
       T[r * kCB + t] = a;
     }
   }
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
           if (sv_s[mid] <= j + Q) bend = mid + 1; else bh2 = mid;
         }
         const float4* Hr = T + r * kCB;
-        for (int bb = blo; bb < bend; ++bb) a4 = fma4(Nv_s[bb * NQ + (j - sv_s[bb] + Q)], Hr[bb], a4);
+        for (int bb = blo; bb < bend; ++bb) a4 = fma4v(Nv_s[bb * NQ + (j - sv_s[bb] + Q)], Hr[bb], a4);
       }
       if (prm.direct) {
         // epilogue (Eq.8/9): dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
