@@ -168,6 +168,7 @@ int launch(const Geo& g, bool bwd, const float* ctrl, float* out, const float* g
   prm.NRB = pl.NRB;
   prm.NCB = pl.NCB;
   prm.T_rows = pl.T_rows;
+  prm.CBW = g.c.n < nb::kBandCols ? g.c.n : nb::kBandCols;
   prm.direct = pl.direct;
   const void* io = bwd ? static_cast<const void*>(gout) : static_cast<const void*>(out);
   prm.bulk = (g.c.ns % 4 == 0) && aligned16(io) ? 1 : 0;

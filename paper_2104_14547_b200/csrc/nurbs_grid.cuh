@@ -60,7 +60,7 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
 }
 
 template <int P, int Q, bool BWD, bool BULK>
-__global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params prm) {
+__global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const Params prm) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   const int warp = tid >> 5;
   const Dir& R = prm.r;
   const Dir& C = prm.c;
+  const int m = C.n;
 
   // ---- decode the tile
   int bid = blockIdx.x;
@@ -83,26 +84,29 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   const int band_rows = S1 - band_lo;            // <= T_rows
   const float* Uk = (P > 0) ? R.knots + (long long)s * R.kstride : nullptr;
   const float* Vk = C.tspan ? nullptr : C.knots + (long long)s * C.kstride;
+  const float4* __restrict__ ctrl_s = prm.ctrl + (size_t)s * R.n * m;
 
-  // ---- shared memory carve-up
-  float4* T = reinterpret_cast<float4*>(smem);                       // [T_rows][kCB] (T, then H)
-  float* stage = reinterpret_cast<float*>(T + (size_t)prm.T_rows * kCB);  // [kStages][kRPS*kCB*3]
-  int* su_s = reinterpret_cast<int*>(stage + kStages * kRPS * kCB * 3);   // [kRowChunk]
-  float* Nu_s = reinterpret_cast<float*>(su_s + kRowChunk);               // [kRowChunk][NP]
-  int* sv_s = reinterpret_cast<int*>(Nu_s + kRowChunk * NP);              // [kCB]      (bwd only)
-  float* Nv_s = reinterpret_cast<float*>(sv_s + kCB);                     // [kCB][NQ]  (bwd only)
-  unsigned char* after = BWD ? reinterpret_cast<unsigned char*>(Nv_s + kCB * NQ)
-                             : reinterpret_cast<unsigned char*>(sv_s);
-  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(after) + 7) & ~uintptr_t(7));
+  // ---- shared memory carve-up (sizes: grid_smem_bytes)
+  float4* cband = reinterpret_cast<float4*>(smem);                           // [T_rows][CBW]
+  float* stage = reinterpret_cast<float*>(cband + (size_t)prm.T_rows * prm.CBW); // [kStages][kRPS*kCB*3]
+  float4* Hring = reinterpret_cast<float4*>(stage + kStages * kRPS * kCB * 3);   // [kHRing][kCB] (bwd)
+  int* su_s = reinterpret_cast<int*>(Hring + (BWD ? kHRing * kCB : 0));          // [kRowChunk]
+  float* Nu_s = reinterpret_cast<float*>(su_s + kRowChunk);                      // [kRowChunk][NP]
+  int* sv_s = reinterpret_cast<int*>(Nu_s + kRowChunk * NP);                     // [kCB]      (bwd)
+  float* Nv_s = reinterpret_cast<float*>(sv_s + kCB);                            // [kCB][NQ]  (bwd)
+  int* misc = reinterpret_cast<int*>(BWD ? Nv_s + kCB * NQ : reinterpret_cast<float*>(sv_s));  // [4]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(misc + 4);                        // 8-byte aligned
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
+  uint64_t* band_bar = bars + 2 * kStages;
 
-  if (BULK && tid == 0) {
+  if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < kStages; ++i) {
       mbar_init(full + i, BWD ? 1u : (uint32_t)kCompute);
       mbar_init(empty + i, BWD ? (uint32_t)kCompute : 1u);
     }
+    mbar_init(band_bar, 1u);
     fence_mbar_init();
   }
 
@@ -127,9 +131,33 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   const int nstage = (nwalk + kRPS - 1) / kRPS;
   const bool contig = (cols == C.ns);  // whole sample rows: consecutive rows are contiguous
 
-  // ======================================================== producer warp (TMA bulk)
-  // Stage slot = kRPS rows at a fixed smem row stride of kCB*3 floats.
+  // ======================================================== producer warp
+  // 1) the control band (rows [band_lo, S1), columns [jlo, jhi] of this column block) into
+  //    smem with TMA bulk copies; 2) the dL/dS stage ring (bwd) or the output drain (fwd).
   if (warp == kCompute / 32) {
+    if ((tid & 31) == 0) {
+      auto cspan = [&](int bb) -> int {
+        int sp = C.tspan ? __ldg(C.tspan + bb) : d_find_span(Vk, m, Q, __ldg(C.s + bb));
+        return min(max(sp, Q), m - 1);
+      };
+      const int jlo = cspan(B0) - Q;
+      const int ncol = cspan(B0 + cols - 1) - jlo + 1;
+      const int use_smem = ncol <= prm.CBW;
+      misc[0] = jlo;
+      misc[1] = use_smem;
+      if (use_smem) {
+        const uint32_t rowb = (uint32_t)ncol * 16u;
+        mbar_arrive_expect_tx(band_bar, rowb * band_rows);
+        const float4* src = ctrl_s + (size_t)band_lo * m + jlo;
+        if (ncol == m && ncol == prm.CBW) {
+          bulk_g2s(cband, src, rowb * band_rows, band_bar);
+        } else {
+          for (int r = 0; r < band_rows; ++r) bulk_g2s(cband + r * prm.CBW, src + (size_t)r * m, rowb, band_bar);
+        }
+      } else {
+        mbar_arrive(band_bar);
+      }
+    }
     if (BULK && (tid & 31) == 0) {
       const uint32_t rowbytes = (uint32_t)cols * 12u;
       const bool one_copy = contig && cols == kCB;  // the stage's rows are one contiguous span
@@ -172,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   const bool valid = t < cols;
   const int b = B0 + (valid ? t : cols - 1);
 
-  // ---- column span + basis (registers), shared with the B2 stage in smem
+  // ---- column span + basis (registers); the backward also needs them in smem for B2
   int sv;
   float nv[Q + 1];
   if (C.tspan) {
@@ -182,32 +210,84 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
     for (int h = 0; h <= Q; ++h) nv[h] = __ldg(tn + h);
   } else {
     const float vb = __ldg(C.s + b);
-    sv = d_find_span(Vk, C.n, Q, vb);
+    sv = d_find_span(Vk, m, Q, vb);
     d_basis<Q>(Vk, sv, vb, Q, nv);
   }
-  sv = min(max(sv, Q), C.n - 1);
+  sv = min(max(sv, Q), m - 1);
   if constexpr (BWD) {
     sv_s[t] = sv;
 #pragma unroll
     for (int h = 0; h < NQ; ++h) Nv_s[t * NQ + h] = h <= Q ? nv[h <= Q ? h : 0] : 0.f;
   }
 
-  // ---- F1: T[r][t] = sum_h Nv[h] Q[band_lo + r][sv - q + h]
-  const float4* __restrict__ ctrl_s = prm.ctrl + (size_t)s * R.n * C.n;
-  {
-    const float4* colp = ctrl_s + (size_t)band_lo * C.n + (sv - Q);
-#pragma unroll 4
-    for (int r = 0; r < band_rows; ++r) {
-      const float4* rowp = colp + (size_t)r * C.n;
-      float4 c[Q + 1];
+  // ---- F1 on demand: T(i) = sum_h Nv[h] Q[i][sv - q + h]  (P:140 homogeneous points)
+  mbar_wait(band_bar, 0);
+  const int jlo = misc[0];
+  const bool band_in_smem = misc[1] != 0;
+  const float4* crow0 = band_in_smem ? cband + (sv - Q - jlo) - (size_t)band_lo * prm.CBW
+                                     : ctrl_s + (sv - Q);
+  const int crow_stride = band_in_smem ? prm.CBW : m;
+  auto Trow = [&](int i) -> float4 {
+    const float4* src = crow0 + (size_t)i * crow_stride;
+    float4 c[Q + 1];
+    if (band_in_smem) {
 #pragma unroll
-      for (int h = 0; h <= Q; ++h) c[h] = __ldg(rowp + h);
-      float4 a = f4(0.f);
+      for (int h = 0; h <= Q; ++h) c[h] = src[h];
+    } else {
 #pragma unroll
-      for (int h = 0; h <= Q; ++h) a = fma4v(nv[h], homog(c[h]), a);
-      T[r * kCB + t] = a;
+      for (int h = 0; h <= Q; ++h) c[h] = __ldg(src + h);
     }
-  }
+    float4 a = f4(0.f);
+#pragma unroll
+    for (int h = 0; h <= Q; ++h) a = fma4v(nv[h], homog(c[h]), a);
+    return a;
+  };
+
+  // ---- B2 over a batch of completed rows [i0, i0+nb) held in the H ring (backward only)
+  auto b2_batch = [&](int i0, int nb) {
+    bar_compute();  // H rows of the batch written by every thread
+    const int jb0 = sv_s[0] - Q;
+    const int jb1 = sv_s[cols - 1];
+    const int nj = prm.direct ? m : jb1 - jb0 + 1;
+    const int jstart = prm.direct ? 0 : jb0;
+    const int ntask = nb * nj;
+    float4* gctrl_s = prm.gctrl + (size_t)s * R.n * m;
+    for (int task = t; task < ntask; task += kCompute) {
+      const int rr = task / nj;
+      const int j = jstart + (task - rr * nj);
+      const int i = i0 + rr;
+      float4 a4 = f4(0.f);
+      if (j >= jb0 && j <= jb1) {
+        int blo = 0, bhi = cols;  // first b with sv >= j
+        while (blo < bhi) {
+          const int mid = (blo + bhi) >> 1;
+          if (sv_s[mid] < j) blo = mid + 1; else bhi = mid;
+        }
+        int bend = blo, bh2 = cols;  // first b with sv > j + q
+        while (bend < bh2) {
+          const int mid = (bend + bh2) >> 1;
+          if (sv_s[mid] <= j + Q) bend = mid + 1; else bh2 = mid;
+        }
+        const float4* Hr = Hring + ((i - band_lo) & (kHRing - 1)) * kCB;
+        for (int bb = blo; bb < bend; ++bb) a4 = fma4v(Nv_s[bb * NQ + (j - sv_s[bb] + Q)], Hr[bb], a4);
+      }
+      if (prm.direct) {
+        // epilogue (Eq.8/9): dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
+        const float4 c = __ldg(ctrl_s + (size_t)i * m + j);
+        gctrl_s[(size_t)i * m + j] =
+            make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
+      } else {
+        prm.slots[((((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows + (i - band_lo)) * m + j] = a4;
+      }
+    }
+    bar_compute();  // ring slots free again
+  };
+  // row i complete (uniform across the CTA): H(i) -> ring; reduce the ring when it is full
+  auto flush_row = [&](int i, float4 h) {
+    const int slotH = (i - band_lo) & (kHRing - 1);
+    Hring[slotH * kCB + t] = h;
+    if (slotH == kHRing - 1) b2_batch(i - (kHRing - 1), kHRing);
+  };
 
   // ---- walk the sample rows: rolling window of P+1 control rows [lo, lo+P]
   float4 tw[P + 1];
@@ -215,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   int lo = band_lo;
 #pragma unroll
   for (int k = 0; k <= P; ++k) {
-    tw[k] = T[k * kCB + t];
+    tw[k] = Trow(band_lo + k);
     acc[k] = f4(0.f);
   }
 
@@ -231,15 +311,15 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   auto row_step = [&](int ci, float* io) {
     const int target = su_s[ci] - P;
     if (target != lo) {
-      do {  // row lo is complete: in the backward it becomes H row lo (aliases T row lo)
-        if constexpr (BWD) T[(lo - band_lo) * kCB + t] = acc[0];
+      do {  // row lo is complete
+        if constexpr (BWD) flush_row(lo, acc[0]);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           tw[k] = tw[k + 1];
           if constexpr (BWD) acc[k] = acc[k + 1];
         }
         ++lo;
-        tw[P] = T[(lo + P - band_lo) * kCB + t];
+        tw[P] = Trow(lo + P);
         if constexpr (BWD) acc[P] = f4(0.f);
       } while (lo < target);
     }
@@ -312,52 +392,14 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
   }
 
   if constexpr (BWD) {
-    // ---- B1 epilogue: flush the last window, zero the rows never reached
+    // ---- B1 epilogue: flush the last window and the rows never reached (zeros), in order
 #pragma unroll
-    for (int k = 0; k <= P; ++k) T[(lo + k - band_lo) * kCB + t] = acc[k];
-    for (int r = lo + P + 1 - band_lo; r < band_rows; ++r) T[r * kCB + t] = f4(0.f);
-    bar_compute();
+    for (int k = 0; k <= P; ++k) flush_row(lo + k, acc[k]);
+    for (int i = lo + P + 1; i < S1; ++i) flush_row(i, f4(0.f));
+    const int done = (S1 - band_lo) & ~(kHRing - 1);  // rows already reduced in full batches
+    if (done < band_rows) b2_batch(band_lo + done, band_rows - done);
 
-    // ---- B2: dQ[i][j] = sum_b H[i-band_lo][b] Nv[b][j - sv(b) + q], b ascending
-    const int j0 = sv_s[0] - Q;
-    const int j1 = sv_s[cols - 1];
-    const int nj = j1 - j0 + 1;
-    float4* gctrl_s = prm.gctrl + (size_t)s * R.n * C.n;
-    const int ntask = prm.direct ? R.n * C.n : band_rows * nj;
-    for (int task = t; task < ntask; task += kCompute) {
-      int r, j;
-      if (prm.direct) {
-        r = task / C.n;  // band_lo == 0 and band_rows == R.n in direct mode
-        j = task - r * C.n;
-      } else {
-        r = task / nj;
-        j = j0 + (task - r * nj);
-      }
-      float4 a4 = f4(0.f);
-      if (j >= j0 && j <= j1) {
-        int blo = 0, bhi = cols;  // first b with sv >= j
-        while (blo < bhi) {
-          const int mid = (blo + bhi) >> 1;
-          if (sv_s[mid] < j) blo = mid + 1; else bhi = mid;
-        }
-        int bend = blo, bh2 = cols;  // first b with sv > j + q
-        while (bend < bh2) {
-          const int mid = (bend + bh2) >> 1;
-          if (sv_s[mid] <= j + Q) bend = mid + 1; else bh2 = mid;
-        }
-        const float4* Hr = T + r * kCB;
-        for (int bb = blo; bb < bend; ++bb) a4 = fma4v(Nv_s[bb * NQ + (j - sv_s[bb] + Q)], Hr[bb], a4);
-      }
-      if (prm.direct) {
-        // epilogue (Eq.8/9): dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
-        const float4 c = __ldg(ctrl_s + (size_t)r * C.n + j);
-        gctrl_s[(size_t)r * C.n + j] =
-            make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
-      } else {
-        prm.slots[((((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows + r) * C.n + j] = a4;
-      }
-    }
-    if (!prm.direct && rb == 0 && t == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(j0, j1);
+    if (!prm.direct && rb == 0 && t == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sv_s[0] - Q, sv_s[cols - 1]);
     if (prm.direct) {  // knot gradients are zero by definition
       if (prm.gR && s < prm.gR_items)
         for (int x = t; x < prm.gR_per; x += kCompute) prm.gR[(size_t)s * prm.gR_per + x] = 0.f;
@@ -369,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 4) nurbs_grid_kernel(const Params pr
 
 template <int P, int Q, bool BWD, bool BULK>
 static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
-  const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows);
+  const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows, prm.CBW);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, BULK>,

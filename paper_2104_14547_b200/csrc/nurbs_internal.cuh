@@ -18,7 +18,9 @@ constexpr int kRPS = 8;           // sample rows per pipeline stage
 constexpr int kStages = 2;        // pipeline depth (stage ring)
 constexpr int kRowChunk = 64;     // rows whose span/basis are staged in smem at once
 constexpr int kMaxQ = 5;          // max column degree (runtime q)
-constexpr int kRMax = 16;         // max control rows in a row-block band (T/H smem rows)
+constexpr int kRMax = 16;         // max control rows in a row-block band
+constexpr int kBandCols = 32;     // smem capacity (columns) of the staged control band
+constexpr int kHRing = 8;         // completed-H rows buffered before a B2 batch (power of 2)
 constexpr int kTargetCTAs = 592;  // 4 resident CTAs x 148 SMs: planning target (fixed so the
                                   // plan, hence summation order, is a pure function of shape)
 
@@ -46,7 +48,8 @@ struct Params {
   float* gC; int gC_per; int gC_items;   // (cols direction)
   int K;                    // knot spans per row block
   int NRB, NCB;             // row blocks, column blocks
-  int T_rows;               // smem rows of T/H = slot rows
+  int T_rows;               // control rows of a row-block band = slot rows
+  int CBW;                  // smem columns of the staged control band (min(m, kBandCols))
   int bulk;                 // 1: TMA bulk staging of out / grad_out
   int direct;               // 1: bwd writes grad_ctrl in-kernel (NRB == NCB == 1)
   float4* slots;            // [B][NRB][NCB][T_rows][c.n] partial dQ (direct == 0)
@@ -117,7 +120,7 @@ cudaError_t launch_tables(const Dir& r, const Dir& c, void* tables, const TabLay
 cudaError_t launch_validate(int B, const Dir& r, const Dir& c, int check_rows,
                             const float4* ctrl, long long n_ctrl,
                             unsigned long long* status, cudaStream_t st);
-size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows);
+size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW);
 
 }  // namespace nb
 

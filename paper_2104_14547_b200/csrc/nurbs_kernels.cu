@@ -123,13 +123,14 @@ __global__ void nurbs_validate_kernel(int B, Dir R, Dir C, int check_rows, const
 }
 
 // ------------------------------------------------------------------------ launchers
-size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows) {
+size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW) {
   const int NP = (P + 1) <= 4 ? 4 : 8;
   const int NQ = (q + 1) <= 4 ? 4 : 8;
-  size_t b = (size_t)T_rows * kCB * 16 + (size_t)kStages * kRPS * kCB * 3 * 4 + kRowChunk * 4 +
+  size_t b = (size_t)T_rows * CBW * 16 + (size_t)kStages * kRPS * kCB * 3 * 4 + kRowChunk * 4 +
              (size_t)kRowChunk * NP * 4;
-  if (bwd) b += kCB * 4 + (size_t)kCB * NQ * 4;
-  b = (b + 7) / 8 * 8 + 2 * kStages * 8;
+  if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4;
+  b += 4 * 4;                                  // misc
+  b = (b + 7) / 8 * 8 + (2 * kStages + 1) * 8;  // mbarriers
   return b;
 }
 
