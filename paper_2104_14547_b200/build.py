@@ -9,13 +9,14 @@ from __future__ import annotations
 
 import glob
 import os
+import shutil
+import tempfile
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libnurbs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc")
 
@@ -39,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     stale = force or not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in deps())
     if not stale:
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    OBJ = tempfile.mkdtemp(prefix="nurbs_b200_obj_")
     procs = []
     for name, src, extra in units():
         obj = os.path.join(OBJ, name + ".o")
@@ -61,6 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
     os.replace(LIB + ".tmp", LIB)
+    shutil.rmtree(OBJ, ignore_errors=True)
     return LIB
 
 

@@ -59,6 +59,105 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
   }
 }
 
+// ---- B2 of the backward for a batch of completed control rows [i0, i0+nb) held in the H
+// ring: dQ[i][j] = sum_b H[i][b] Nv[b][j - sv(b) + q] in ascending b, then the Eq.8/9
+// epilogue (direct mode) or the tile partial (cross-tile reduce). Called by the 128 compute
+// threads together (uniform), rarely (once per kB2Batch rows, outside the unrolled row loop).
+struct B2Args {
+  const float4* Hring;
+  const float* Nv_s;
+  const int* sv_s;
+  const int* sst;
+  const float4* ctrl_s;   // this surface's control net
+  float4* gctrl_s;        // this surface's gradient (direct mode)
+  float4* slots;          // this tile's partial slot [T_rows][m] (reduce mode)
+  int m, cols, band_lo, sfirst, nspan;
+  bool fast, direct;
+};
+
+template <int Q>
+__device__ __forceinline__ void b2_batch_fn(const B2Args* __restrict__ ap, int i0, int nb) {
+  constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;
+  bar_compute();          // H rows of the batch (and *ap) written by every thread
+  const B2Args a = *ap;  // CTA-uniform arguments live in smem, not in the walk's registers
+  const int t = threadIdx.x, m = a.m;
+  auto store_dq = [&](int i, int j, float4 a4) {
+    if (a.direct) {  // dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
+      const float4 c = __ldg(a.ctrl_s + (size_t)i * m + j);
+      a.gctrl_s[(size_t)i * m + j] =
+          make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
+    } else {
+      a.slots[(size_t)(i - a.band_lo) * m + j] = a4;
+    }
+  };
+  if (a.fast) {  // one warp per control row, one lane per knot span of the column block
+    const int lane = t & 31;
+    for (int rr = (t >> 5); rr < nb; rr += kCompute / 32) {
+      const int i = i0 + rr;
+      const float4* Hr = a.Hring + ((i - a.band_lo) & (kHRing - 1)) * kCB;
+      float4 c[Q + 1];
+#pragma unroll
+      for (int h = 0; h <= Q; ++h) c[h] = f4(0.f);
+      if (lane < a.nspan) {  // lane k: span sfirst + k, columns [sst[k], sst[k+1])
+        const int e = a.sst[lane + 1];
+        for (int bb = a.sst[lane]; bb < e; ++bb) {
+          const float4 hv = Hr[bb];
+          float nvv[NQ];
+          const float4 q0 = *reinterpret_cast<const float4*>(a.Nv_s + bb * NQ);
+          nvv[0] = q0.x; nvv[1] = q0.y; nvv[2] = q0.z; nvv[3] = q0.w;
+          if constexpr (NQ == 8) {
+            const float4 q1 = *reinterpret_cast<const float4*>(a.Nv_s + bb * NQ + 4);
+            nvv[4] = q1.x; nvv[5] = q1.y; nvv[6] = q1.z; nvv[7] = q1.w;
+          }
+#pragma unroll
+          for (int h = 0; h <= Q; ++h) c[h] = fma4v(nvv[h], hv, c[h]);
+        }
+      }
+      // lane L collects column j = sfirst - q + L: sum_h c[h] of lane L - h (span j + q - h)
+      float4 d = f4(0.f);
+#pragma unroll
+      for (int h = 0; h <= Q; ++h) {
+        const float vx = __shfl_up_sync(0xffffffffu, c[h].x, h);
+        const float vy = __shfl_up_sync(0xffffffffu, c[h].y, h);
+        const float vz = __shfl_up_sync(0xffffffffu, c[h].z, h);
+        const float vw = __shfl_up_sync(0xffffffffu, c[h].w, h);
+        if (lane >= h) d = make_float4(d.x + vx, d.y + vy, d.z + vz, d.w + vw);
+      }
+      if (lane < a.nspan + Q) store_dq(i, a.sfirst - Q + lane, d);
+      if (a.direct)  // columns this block does not touch
+        for (int j = lane; j < m; j += 32)
+          if (j < a.sfirst - Q || j >= a.sfirst + a.nspan) store_dq(i, j, f4(0.f));
+    }
+  } else {  // many spans in one block (dense knots): one (row, column) task per thread
+    const int jb0 = a.sfirst - Q;
+    const int jb1 = a.sfirst + a.nspan - 1;
+    const int nj = a.direct ? m : jb1 - jb0 + 1;
+    const int jstart = a.direct ? 0 : jb0;
+    for (int task = t; task < nb * nj; task += kCompute) {
+      const int rr = task / nj;
+      const int j = jstart + (task - rr * nj);
+      const int i = i0 + rr;
+      float4 a4 = f4(0.f);
+      if (j >= jb0 && j <= jb1) {
+        int blo = 0, bhi = a.cols;  // first b with sv >= j
+        while (blo < bhi) {
+          const int mid = (blo + bhi) >> 1;
+          if (a.sv_s[mid] < j) blo = mid + 1; else bhi = mid;
+        }
+        int bend = blo, bh2 = a.cols;  // first b with sv > j + q
+        while (bend < bh2) {
+          const int mid = (bend + bh2) >> 1;
+          if (a.sv_s[mid] <= j + Q) bend = mid + 1; else bh2 = mid;
+        }
+        const float4* Hr = a.Hring + ((i - a.band_lo) & (kHRing - 1)) * kCB;
+        for (int bb = blo; bb < bend; ++bb) a4 = fma4v(a.Nv_s[bb * NQ + (j - a.sv_s[bb] + Q)], Hr[bb], a4);
+      }
+      store_dq(i, j, a4);
+    }
+  }
+  bar_compute();  // ring slots free again
+}
+
 template <int P, int Q, bool BWD, bool BULK>
 __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const Params prm) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -94,8 +193,11 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   float* Nu_s = reinterpret_cast<float*>(su_s + kRowChunk);                      // [kRowChunk][NP]
   int* sv_s = reinterpret_cast<int*>(Nu_s + kRowChunk * NP);                     // [kCB]      (bwd)
   float* Nv_s = reinterpret_cast<float*>(sv_s + kCB);                            // [kCB][NQ]  (bwd)
-  int* misc = reinterpret_cast<int*>(BWD ? Nv_s + kCB * NQ : reinterpret_cast<float*>(sv_s));  // [4]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(misc + 4);                        // 8-byte aligned
+  int* sst = reinterpret_cast<int*>(Nv_s + kCB * NQ);                            // [kCB+4]    (bwd)
+  int* misc = BWD ? sst + kCB + 4 : sv_s;                                        // [4]
+  B2Args* b2args = reinterpret_cast<B2Args*>(misc + 4);                         // 16-byte aligned (bwd)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(b2args) +
+                                               (BWD ? sizeof(B2Args) : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* band_bar = bars + 2 * kStages;
@@ -227,6 +329,27 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   const float4* crow0 = band_in_smem ? cband + (sv - Q - jlo) - (size_t)band_lo * prm.CBW
                                      : ctrl_s + (sv - Q);
   const int crow_stride = band_in_smem ? prm.CBW : m;
+
+  // ---- backward: knot spans present in this column block. B2 runs one warp per control row
+  // with one lane per span when the block touches at most 32 - q consecutive spans.
+  int sfirst = 0, nspan = 0;
+  bool b2fast = false;
+  if constexpr (BWD) {
+    bar_compute();  // sv_s / Nv_s complete
+    sfirst = sv_s[0];
+    nspan = sv_s[cols - 1] - sfirst + 1;
+    b2fast = nspan + Q <= 32;
+    if (b2fast) {
+      for (int k = t; k <= nspan; k += kCompute) {  // sst[k] = first b with sv(b) >= sfirst + k
+        int lo2 = 0, hi2 = cols;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (sv_s[mid] < sfirst + k) lo2 = mid + 1; else hi2 = mid;
+        }
+        sst[k] = lo2;
+      }
+    }
+  }
   auto Trow = [&](int i) -> float4 {
     const float4* src = crow0 + (size_t)i * crow_stride;
     float4 c[Q + 1];
@@ -243,50 +366,26 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
     return a;
   };
 
-  // ---- B2 over a batch of completed rows [i0, i0+nb) held in the H ring (backward only)
-  auto b2_batch = [&](int i0, int nb) {
-    bar_compute();  // H rows of the batch written by every thread
-    const int jb0 = sv_s[0] - Q;
-    const int jb1 = sv_s[cols - 1];
-    const int nj = prm.direct ? m : jb1 - jb0 + 1;
-    const int jstart = prm.direct ? 0 : jb0;
-    const int ntask = nb * nj;
-    float4* gctrl_s = prm.gctrl + (size_t)s * R.n * m;
-    for (int task = t; task < ntask; task += kCompute) {
-      const int rr = task / nj;
-      const int j = jstart + (task - rr * nj);
-      const int i = i0 + rr;
-      float4 a4 = f4(0.f);
-      if (j >= jb0 && j <= jb1) {
-        int blo = 0, bhi = cols;  // first b with sv >= j
-        while (blo < bhi) {
-          const int mid = (blo + bhi) >> 1;
-          if (sv_s[mid] < j) blo = mid + 1; else bhi = mid;
-        }
-        int bend = blo, bh2 = cols;  // first b with sv > j + q
-        while (bend < bh2) {
-          const int mid = (bend + bh2) >> 1;
-          if (sv_s[mid] <= j + Q) bend = mid + 1; else bh2 = mid;
-        }
-        const float4* Hr = Hring + ((i - band_lo) & (kHRing - 1)) * kCB;
-        for (int bb = blo; bb < bend; ++bb) a4 = fma4v(Nv_s[bb * NQ + (j - sv_s[bb] + Q)], Hr[bb], a4);
-      }
-      if (prm.direct) {
-        // epilogue (Eq.8/9): dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
-        const float4 c = __ldg(ctrl_s + (size_t)i * m + j);
-        gctrl_s[(size_t)i * m + j] =
-            make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
-      } else {
-        prm.slots[((((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows + (i - band_lo)) * m + j] = a4;
-      }
+  // ---- B2 (backward): batches of completed rows in the H ring -> dQ (b2_batch_fn)
+  if (BWD && t == 0) {
+    B2Args& b2a = *b2args;
+    b2a.Hring = Hring; b2a.Nv_s = Nv_s; b2a.sv_s = sv_s; b2a.sst = sst;
+    b2a.ctrl_s = ctrl_s; b2a.gctrl_s = prm.gctrl + (size_t)s * R.n * m;
+    b2a.slots = prm.slots ? prm.slots + (((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows * m : nullptr;
+    b2a.m = m; b2a.cols = cols; b2a.band_lo = band_lo; b2a.sfirst = sfirst; b2a.nspan = nspan;
+    b2a.fast = b2fast; b2a.direct = prm.direct;
+  }
+  auto b2_batch = [&](int i0, int nb) { b2_batch_fn<Q>(b2args, i0, nb); };
+  int b2_next = band_lo;  // first completed control row not yet reduced by B2
+  // row i complete (uniform across the CTA): H(i) -> ring. The fast variant never reduces
+  // (the stage loop guarantees ring capacity); the checked one reduces a full ring.
+  auto flush_fast = [&](int i, float4 h) { Hring[((i - band_lo) & (kHRing - 1)) * kCB + t] = h; };
+  auto flush_checked = [&](int i, float4 h) {
+    flush_fast(i, h);
+    if (i + 1 - b2_next == kHRing) {
+      b2_batch(b2_next, kHRing);
+      b2_next += kHRing;
     }
-    bar_compute();  // ring slots free again
-  };
-  // row i complete (uniform across the CTA): H(i) -> ring; reduce the ring when it is full
-  auto flush_row = [&](int i, float4 h) {
-    const int slotH = (i - band_lo) & (kHRing - 1);
-    Hring[slotH * kCB + t] = h;
-    if (slotH == kHRing - 1) b2_batch(i - (kHRing - 1), kHRing);
   };
 
   // ---- walk the sample rows: rolling window of P+1 control rows [lo, lo+P]
@@ -308,11 +407,11 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
 
   // One row of the walk: advance the window to the row's span if it changed (uniform across
   // the CTA, rare: once per knot span), then F2 (+ B1). ci = row index in the smem tables.
-  auto row_step = [&](int ci, float* io) {
+  auto row_step = [&](int ci, float* io, auto flush) {
     const int target = su_s[ci] - P;
     if (target != lo) {
       do {  // row lo is complete
-        if constexpr (BWD) flush_row(lo, acc[0]);
+        if constexpr (BWD) flush(lo, acc[0]);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           tw[k] = tw[k + 1];
@@ -332,6 +431,26 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
       nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
     }
     walk_row<P, BWD>(nu, tw, acc, io, BULK && !BWD ? true : valid);
+  };
+  // rows [r0, r0+nr) of the walk: unrolled fast path when the H ring cannot overflow
+  auto run_rows = [&](int ci0, int nr, float* io0, size_t io_stride) {
+    bool fast = nr == kRPS;
+    if constexpr (BWD) {  // rows completed by this stage = advance of the window
+      const int lo_end = max(lo, su_s[ci0 + nr - 1] - P);
+      fast = fast && (lo_end - b2_next) <= kHRing;
+    }
+    if (fast) {
+#pragma unroll
+      for (int r = 0; r < kRPS; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_fast);
+    } else {
+      for (int r = 0; r < nr; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_checked);
+    }
+    if constexpr (BWD) {
+      while (lo - b2_next >= kB2Batch) {
+        b2_batch(b2_next, kB2Batch);
+        b2_next += kB2Batch;
+      }
+    }
   };
 
   int slot = 0, use = 0;
@@ -370,23 +489,11 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
     if constexpr (BULK) {
       if (BWD) mbar_wait(full + slot, use & 1);
       else if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
-      float* buf = stage + slot * (kRPS * kCB * 3) + t * 3;
-      if (nr == kRPS) {
-#pragma unroll
-        for (int r = 0; r < kRPS; ++r) row_step(ci0 + r, buf + r * kCB * 3);
-      } else {
-        for (int r = 0; r < nr; ++r) row_step(ci0 + r, buf + r * kCB * 3);
-      }
+      run_rows(ci0, nr, stage + slot * (kRPS * kCB * 3) + t * 3, (size_t)kCB * 3);
       if constexpr (!BWD) fence_proxy_async();
       mbar_arrive(BWD ? empty + slot : full + slot);
     } else {
-      float* io = gio + (size_t)r0 * grow;
-      if (nr == kRPS) {
-#pragma unroll
-        for (int r = 0; r < kRPS; ++r) row_step(ci0 + r, io + r * grow);
-      } else {
-        for (int r = 0; r < nr; ++r) row_step(ci0 + r, io + r * grow);
-      }
+      run_rows(ci0, nr, gio + (size_t)r0 * grow, grow);
     }
     if (++slot == kStages) { slot = 0; ++use; }
   }
@@ -394,12 +501,11 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   if constexpr (BWD) {
     // ---- B1 epilogue: flush the last window and the rows never reached (zeros), in order
 #pragma unroll
-    for (int k = 0; k <= P; ++k) flush_row(lo + k, acc[k]);
-    for (int i = lo + P + 1; i < S1; ++i) flush_row(i, f4(0.f));
-    const int done = (S1 - band_lo) & ~(kHRing - 1);  // rows already reduced in full batches
-    if (done < band_rows) b2_batch(band_lo + done, band_rows - done);
+    for (int k = 0; k <= P; ++k) flush_checked(lo + k, acc[k]);
+    for (int i = lo + P + 1; i < S1; ++i) flush_checked(i, f4(0.f));
+    if (b2_next < S1) b2_batch(b2_next, S1 - b2_next);
 
-    if (!prm.direct && rb == 0 && t == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sv_s[0] - Q, sv_s[cols - 1]);
+    if (!prm.direct && rb == 0 && t == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sfirst - Q, sfirst + nspan - 1);
     if (prm.direct) {  // knot gradients are zero by definition
       if (prm.gR && s < prm.gR_items)
         for (int x = t; x < prm.gR_per; x += kCompute) prm.gR[(size_t)s * prm.gR_per + x] = 0.f;

@@ -20,7 +20,8 @@ constexpr int kRowChunk = 64;     // rows whose span/basis are staged in smem at
 constexpr int kMaxQ = 5;          // max column degree (runtime q)
 constexpr int kRMax = 16;         // max control rows in a row-block band
 constexpr int kBandCols = 32;     // smem capacity (columns) of the staged control band
-constexpr int kHRing = 8;         // completed-H rows buffered before a B2 batch (power of 2)
+constexpr int kHRing = 8;         // completed-H rows buffered for B2 (power of 2)
+constexpr int kB2Batch = 4;       // B2 reduces completed rows in batches of this size
 constexpr int kTargetCTAs = 592;  // 4 resident CTAs x 148 SMs: planning target (fixed so the
                                   // plan, hence summation order, is a pure function of shape)
 

@@ -128,8 +128,9 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW) {
   const int NQ = (q + 1) <= 4 ? 4 : 8;
   size_t b = (size_t)T_rows * CBW * 16 + (size_t)kStages * kRPS * kCB * 3 * 4 + kRowChunk * 4 +
              (size_t)kRowChunk * NP * 4;
-  if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4;
+  if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4 + (kCB + 4) * 4;
   b += 4 * 4;                                  // misc
+  if (bwd) b += 128;                           // B2Args (see nurbs_grid.cuh)
   b = (b + 7) / 8 * 8 + (2 * kStages + 1) * 8;  // mbarriers
   return b;
 }
