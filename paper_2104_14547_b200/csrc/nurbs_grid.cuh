@@ -78,7 +78,7 @@ struct B2Args {
 template <int Q>
 __device__ __forceinline__ void b2_batch_fn(const B2Args* __restrict__ ap, int i0, int nb) {
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;
-  bar_compute();          // H rows of the batch (and *ap) written by every thread
+  __syncthreads();        // H rows of the batch (and *ap) written by every thread
   const B2Args a = *ap;  // CTA-uniform arguments live in smem, not in the walk's registers
   const int t = threadIdx.x, m = a.m;
   auto store_dq = [&](int i, int j, float4 a4) {
@@ -155,15 +155,19 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args* __restrict__ ap, int i
       store_dq(i, j, a4);
     }
   }
-  bar_compute();  // ring slots free again
+  __syncthreads();  // ring slots free again
 }
 
 template <int P, int Q, bool BWD, bool BULK>
-__global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const Params prm) {
+__global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const Params prm) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
+  constexpr int RPS = BWD ? kRPS_B : kRPS_F;      // sample rows per pipeline stage
+  constexpr int NST = BWD ? kStages_B : kStages_F;  // stages per warp ring
+  constexpr int SROW = kCB * 3;                    // floats of one staged sample row
   const int tid = threadIdx.x;
+  const int lane = tid & 31;
   const int warp = tid >> 5;
   const Dir& R = prm.r;
   const Dir& C = prm.c;
@@ -186,33 +190,34 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   const float4* __restrict__ ctrl_s = prm.ctrl + (size_t)s * R.n * m;
 
   // ---- shared memory carve-up (sizes: grid_smem_bytes)
-  float4* cband = reinterpret_cast<float4*>(smem);                           // [T_rows][CBW]
-  float* stage = reinterpret_cast<float*>(cband + (size_t)prm.T_rows * prm.CBW); // [kStages][kRPS*kCB*3]
-  float4* Hring = reinterpret_cast<float4*>(stage + kStages * kRPS * kCB * 3);   // [kHRing][kCB] (bwd)
-  int* su_s = reinterpret_cast<int*>(Hring + (BWD ? kHRing * kCB : 0));          // [kRowChunk]
-  float* Nu_s = reinterpret_cast<float*>(su_s + kRowChunk);                      // [kRowChunk][NP]
-  int* sv_s = reinterpret_cast<int*>(Nu_s + kRowChunk * NP);                     // [kCB]      (bwd)
-  float* Nv_s = reinterpret_cast<float*>(sv_s + kCB);                            // [kCB][NQ]  (bwd)
-  int* sst = reinterpret_cast<int*>(Nv_s + kCB * NQ);                            // [kCB+4]    (bwd)
-  int* misc = BWD ? sst + kCB + 4 : sv_s;                                        // [4]
-  B2Args* b2args = reinterpret_cast<B2Args*>(misc + 4);                         // 16-byte aligned (bwd)
+  float4* cband = reinterpret_cast<float4*>(smem);                                 // [T_rows][CBW]
+  float* stage = reinterpret_cast<float*>(cband + (size_t)prm.T_rows * prm.CBW);    // [NST][RPS][SROW]
+  float4* Hring = reinterpret_cast<float4*>(stage + NST * RPS * SROW);              // [kHRing][kCB] (bwd)
+  int* su_s = reinterpret_cast<int*>(Hring + (BWD ? kHRing * kCB : 0));            // [kRowChunk]
+  float* Nu_s = reinterpret_cast<float*>(su_s + kRowChunk);                        // [kRowChunk][NP]
+  int* sv_s = reinterpret_cast<int*>(Nu_s + kRowChunk * NP);                       // [kCB]      (bwd)
+  float* Nv_s = reinterpret_cast<float*>(sv_s + kCB);                              // [kCB][NQ]  (bwd)
+  int* sst = reinterpret_cast<int*>(Nv_s + kCB * NQ);                              // [kCB+4]    (bwd)
+  int* misc = BWD ? sst + kCB + 4 : sv_s;                                          // [4]
+  B2Args* b2args = reinterpret_cast<B2Args*>(misc + 4);                           // (bwd)
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(b2args) +
                                                (BWD ? sizeof(B2Args) : 0));
-  uint64_t* full = bars;
-  uint64_t* empty = bars + kStages;
-  uint64_t* band_bar = bars + 2 * kStages;
+  uint64_t* band_bar = bars;            // control band landed
+  uint64_t* sfull = bars + 1;           // bwd: stage slot filled by TMA (count 1 + tx bytes)
+  uint64_t* sempty = bars + 1 + NST;    // fwd: stage slot drained by TMA (count 1)
+  int* scnt = reinterpret_cast<int*>(bars + 1 + 2 * NST);  // per slot: warps done with the stage
 
   if (tid == 0) {
-#pragma unroll
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(full + i, BWD ? 1u : (uint32_t)kCompute);
-      mbar_init(empty + i, BWD ? (uint32_t)kCompute : 1u);
-    }
     mbar_init(band_bar, 1u);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(sfull + i, 1u);
+      mbar_init(sempty + i, 1u);
+      scnt[i] = 0;
+    }
     fence_mbar_init();
   }
 
-  // ---- sample rows of this row block: spans in [S0, S1)   (all 160 threads)
+  // ---- sample rows of this row block: spans in [S0, S1)
   int a_lo = 0, a_hi = R.ns;
   if (prm.NRB > 1) {
     int s_end = R.n - 1;  // last non-empty span (R3)
@@ -228,81 +233,73 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
     if (rb > 0) a_lo = cta_first_true(R.ns, ge(S0));
     if (rb < prm.NRB - 1) a_hi = cta_first_true(R.ns, ge(S1));
   }
-  __syncthreads();
+  __syncthreads();  // mbarrier init visible
   const int nwalk = max(0, a_hi - a_lo);
-  const int nstage = (nwalk + kRPS - 1) / kRPS;
-  const bool contig = (cols == C.ns);  // whole sample rows: consecutive rows are contiguous
+  const int nstage = (nwalk + RPS - 1) / RPS;
 
-  // ======================================================== producer warp
-  // 1) the control band (rows [band_lo, S1), columns [jlo, jhi] of this column block) into
-  //    smem with TMA bulk copies; 2) the dL/dS stage ring (bwd) or the output drain (fwd).
-  if (warp == kCompute / 32) {
-    if ((tid & 31) == 0) {
-      auto cspan = [&](int bb) -> int {
-        int sp = C.tspan ? __ldg(C.tspan + bb) : d_find_span(Vk, m, Q, __ldg(C.s + bb));
-        return min(max(sp, Q), m - 1);
-      };
-      const int jlo = cspan(B0) - Q;
-      const int ncol = cspan(B0 + cols - 1) - jlo + 1;
-      const int use_smem = ncol <= prm.CBW;
-      misc[0] = jlo;
-      misc[1] = use_smem;
-      if (use_smem) {
-        const uint32_t rowb = (uint32_t)ncol * 16u;
-        mbar_arrive_expect_tx(band_bar, rowb * band_rows);
-        const float4* src = ctrl_s + (size_t)band_lo * m + jlo;
-        if (ncol == m && ncol == prm.CBW) {
-          bulk_g2s(cband, src, rowb * band_rows, band_bar);
-        } else {
-          for (int r = 0; r < band_rows; ++r) bulk_g2s(cband + r * prm.CBW, src + (size_t)r * m, rowb, band_bar);
-        }
+  // ---- thread 0: the control band (rows [band_lo, S1), columns [jlo, jhi] of this column
+  // block) into smem with TMA bulk copies.
+  if (tid == 0) {
+    auto cspan = [&](int bb) -> int {
+      int sp = C.tspan ? __ldg(C.tspan + bb) : d_find_span(Vk, m, Q, __ldg(C.s + bb));
+      return min(max(sp, Q), m - 1);
+    };
+    const int jlo = cspan(B0) - Q;
+    const int ncol = cspan(B0 + cols - 1) - jlo + 1;
+    const int use_smem = ncol <= prm.CBW;
+    misc[0] = jlo;
+    misc[1] = use_smem;
+    if (use_smem) {
+      const uint32_t rowb = (uint32_t)ncol * 16u;
+      mbar_arrive_expect_tx(band_bar, rowb * band_rows);
+      const float4* src = ctrl_s + (size_t)band_lo * m + jlo;
+      if (ncol == m && ncol == prm.CBW) {
+        bulk_g2s(cband, src, rowb * band_rows, band_bar);
       } else {
-        mbar_arrive(band_bar);
+        for (int r = 0; r < band_rows; ++r) bulk_g2s(cband + r * prm.CBW, src + (size_t)r * m, rowb, band_bar);
       }
+    } else {
+      mbar_arrive(band_bar);
     }
-    if (BULK && (tid & 31) == 0) {
-      const uint32_t rowbytes = (uint32_t)cols * 12u;
-      const bool one_copy = contig && cols == kCB;  // the stage's rows are one contiguous span
-      int slot = 0, use = 0;
-      for (int k = 0; k < nstage; ++k) {
-        const int r0 = a_lo + k * kRPS;
-        const int nr = min(kRPS, a_hi - r0);
-        float* buf = stage + slot * (kRPS * kCB * 3);
-        if constexpr (BWD) {
-          if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
-          mbar_arrive_expect_tx(full + slot, rowbytes * nr);
-          const float* src = prm.gout + ((size_t)((size_t)s * R.ns + r0) * C.ns + B0) * 3;
-          if (one_copy) {
-            bulk_g2s(buf, src, rowbytes * nr, full + slot);
-          } else {
-            for (int rr = 0; rr < nr; ++rr)
-              bulk_g2s(buf + rr * kCB * 3, src + (size_t)rr * C.ns * 3, rowbytes, full + slot);
-          }
-        } else {
-          mbar_wait(full + slot, use & 1);
-          float* dst = prm.out + ((size_t)((size_t)s * R.ns + r0) * C.ns + B0) * 3;
-          if (one_copy) {
-            bulk_s2g(dst, buf, rowbytes * nr);
-          } else {
-            for (int rr = 0; rr < nr; ++rr) bulk_s2g(dst + (size_t)rr * C.ns * 3, buf + rr * kCB * 3, rowbytes);
-          }
-          bulk_commit();
-          bulk_wait_read_all();
-          mbar_arrive(empty + slot);
-        }
-        if (++slot == kStages) { slot = 0; ++use; }
-      }
-      if constexpr (!BWD) bulk_wait_all();
-    }
-    return;
   }
 
-  // ======================================================== compute warps (128 threads)
-  const int t = tid;
-  const bool valid = t < cols;
-  const int b = B0 + (valid ? t : cols - 1);
+  // ---- TMA stage pipeline: slot = RPS whole sample rows (cols floats x 3). No producer warp:
+  // the LAST warp to finish a stage (smem counter) issues the TMA for it — the next dL/dS
+  // load into the freed slot (bwd) or the drain of the filled slot to HBM (fwd).
+  const uint32_t rowbytes = (uint32_t)cols * 12u;
+  const bool one_copy = (cols == C.ns) && cols == kCB;  // a stage is one contiguous span
+  const size_t grow = (size_t)C.ns * 3;                 // floats between consecutive rows
+  const size_t g0 = (((size_t)s * R.ns + a_lo) * C.ns + B0) * 3;  // row a_lo, column B0
+  auto issue_load = [&](int k, int slot) {  // bwd, one thread: stage k of dL/dS into `slot`
+    const int nr = min(RPS, nwalk - k * RPS);
+    float* buf = stage + slot * (RPS * SROW);
+    const float* src = prm.gout + g0 + (size_t)k * RPS * grow;
+    mbar_arrive_expect_tx(sfull + slot, rowbytes * nr);
+    if (one_copy) {
+      bulk_g2s(buf, src, rowbytes * nr, sfull + slot);
+    } else {
+      for (int rr = 0; rr < nr; ++rr) bulk_g2s(buf + rr * SROW, src + (size_t)rr * grow, rowbytes, sfull + slot);
+    }
+  };
+  auto issue_store = [&](int k, int slot) {  // fwd, one thread: drain stage k from `slot`
+    const int nr = min(RPS, nwalk - k * RPS);
+    const float* buf = stage + slot * (RPS * SROW);
+    float* dst = prm.out + g0 + (size_t)k * RPS * grow;
+    if (one_copy) {
+      bulk_s2g(dst, buf, rowbytes * nr);
+    } else {
+      for (int rr = 0; rr < nr; ++rr) bulk_s2g(dst + (size_t)rr * grow, buf + rr * SROW, rowbytes);
+    }
+    bulk_commit();
+    bulk_wait_read_all();  // the slot may be rewritten once TMA has read it
+    mbar_arrive(sempty + slot);
+  };
+  if (BWD && BULK && tid == 0)
+    for (int k = 0; k < min(NST, nstage); ++k) issue_load(k, k);
 
   // ---- column span + basis (registers); the backward also needs them in smem for B2
+  const bool valid = tid < cols;
+  const int b = B0 + (valid ? tid : cols - 1);
   int sv;
   float nv[Q + 1];
   if (C.tspan) {
@@ -317,9 +314,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   }
   sv = min(max(sv, Q), m - 1);
   if constexpr (BWD) {
-    sv_s[t] = sv;
+    sv_s[tid] = sv;
 #pragma unroll
-    for (int h = 0; h < NQ; ++h) Nv_s[t * NQ + h] = h <= Q ? nv[h <= Q ? h : 0] : 0.f;
+    for (int h = 0; h < NQ; ++h) Nv_s[tid * NQ + h] = h <= Q ? nv[h <= Q ? h : 0] : 0.f;
   }
 
   // ---- F1 on demand: T(i) = sum_h Nv[h] Q[i][sv - q + h]  (P:140 homogeneous points)
@@ -335,12 +332,12 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   int sfirst = 0, nspan = 0;
   bool b2fast = false;
   if constexpr (BWD) {
-    bar_compute();  // sv_s / Nv_s complete
+    __syncthreads();  // sv_s / Nv_s complete
     sfirst = sv_s[0];
     nspan = sv_s[cols - 1] - sfirst + 1;
     b2fast = nspan + Q <= 32;
     if (b2fast) {
-      for (int k = t; k <= nspan; k += kCompute) {  // sst[k] = first b with sv(b) >= sfirst + k
+      for (int k = tid; k <= nspan; k += kThreads) {  // sst[k] = first b with sv(b) >= sfirst + k
         int lo2 = 0, hi2 = cols;
         while (lo2 < hi2) {
           const int mid = (lo2 + hi2) >> 1;
@@ -348,6 +345,14 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
         }
         sst[k] = lo2;
       }
+    }
+    if (tid == 0) {
+      B2Args& b2a = *b2args;
+      b2a.Hring = Hring; b2a.Nv_s = Nv_s; b2a.sv_s = sv_s; b2a.sst = sst;
+      b2a.ctrl_s = ctrl_s; b2a.gctrl_s = prm.gctrl + (size_t)s * R.n * m;
+      b2a.slots = prm.slots ? prm.slots + (((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows * m : nullptr;
+      b2a.m = m; b2a.cols = cols; b2a.band_lo = band_lo; b2a.sfirst = sfirst; b2a.nspan = nspan;
+      b2a.fast = b2fast; b2a.direct = prm.direct;
     }
   }
   auto Trow = [&](int i) -> float4 {
@@ -367,19 +372,11 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   };
 
   // ---- B2 (backward): batches of completed rows in the H ring -> dQ (b2_batch_fn)
-  if (BWD && t == 0) {
-    B2Args& b2a = *b2args;
-    b2a.Hring = Hring; b2a.Nv_s = Nv_s; b2a.sv_s = sv_s; b2a.sst = sst;
-    b2a.ctrl_s = ctrl_s; b2a.gctrl_s = prm.gctrl + (size_t)s * R.n * m;
-    b2a.slots = prm.slots ? prm.slots + (((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows * m : nullptr;
-    b2a.m = m; b2a.cols = cols; b2a.band_lo = band_lo; b2a.sfirst = sfirst; b2a.nspan = nspan;
-    b2a.fast = b2fast; b2a.direct = prm.direct;
-  }
   auto b2_batch = [&](int i0, int nb) { b2_batch_fn<Q>(b2args, i0, nb); };
   int b2_next = band_lo;  // first completed control row not yet reduced by B2
   // row i complete (uniform across the CTA): H(i) -> ring. The fast variant never reduces
   // (the stage loop guarantees ring capacity); the checked one reduces a full ring.
-  auto flush_fast = [&](int i, float4 h) { Hring[((i - band_lo) & (kHRing - 1)) * kCB + t] = h; };
+  auto flush_fast = [&](int i, float4 h) { Hring[((i - band_lo) & (kHRing - 1)) * kCB + tid] = h; };
   auto flush_checked = [&](int i, float4 h) {
     flush_fast(i, h);
     if (i + 1 - b2_next == kHRing) {
@@ -397,13 +394,6 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
     tw[k] = Trow(band_lo + k);
     acc[k] = f4(0.f);
   }
-
-  // direct (non-TMA) path: this thread's element of row a_lo in out / grad_out
-  float* gio = nullptr;
-  if constexpr (!BULK) {
-    gio = (BWD ? const_cast<float*>(prm.gout) : prm.out) + (((size_t)s * R.ns + a_lo) * C.ns + b) * 3;
-  }
-  const size_t grow = (size_t)C.ns * 3;  // floats between consecutive sample rows
 
   // One row of the walk: advance the window to the row's span if it changed (uniform across
   // the CTA, rare: once per knot span), then F2 (+ B1). ci = row index in the smem tables.
@@ -434,14 +424,14 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
   };
   // rows [r0, r0+nr) of the walk: unrolled fast path when the H ring cannot overflow
   auto run_rows = [&](int ci0, int nr, float* io0, size_t io_stride) {
-    bool fast = nr == kRPS;
+    bool fast = nr == RPS;
     if constexpr (BWD) {  // rows completed by this stage = advance of the window
       const int lo_end = max(lo, su_s[ci0 + nr - 1] - P);
       fast = fast && (lo_end - b2_next) <= kHRing;
     }
     if (fast) {
 #pragma unroll
-      for (int r = 0; r < kRPS; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_fast);
+      for (int r = 0; r < RPS; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_fast);
     } else {
       for (int r = 0; r < nr; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_checked);
     }
@@ -453,16 +443,22 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
     }
   };
 
+  // direct (non-TMA) path: this thread's element of row a_lo in out / grad_out
+  float* gio = nullptr;
+  if constexpr (!BULK) {
+    gio = (BWD ? const_cast<float*>(prm.gout) : prm.out) + (((size_t)s * R.ns + a_lo) * C.ns + b) * 3;
+  }
+
   int slot = 0, use = 0;
   for (int st = 0; st < nstage; ++st) {
-    const int r0 = st * kRPS;                 // walk index of the stage's first row
-    const int nr = min(kRPS, nwalk - r0);
-    const int ci0 = r0 % kRowChunk;           // kRowChunk is a multiple of kRPS
+    const int r0 = st * RPS;                  // walk index of the stage's first row
+    const int nr = min(RPS, nwalk - r0);
+    const int ci0 = r0 % kRowChunk;           // kRowChunk is a multiple of RPS
     if (ci0 == 0) {                           // stage span + basis of the next kRowChunk rows
-      if (r0 > 0) bar_compute();              // previous chunk fully consumed
+      if (r0 > 0) __syncthreads();            // previous chunk fully consumed
       const int cn = min(kRowChunk, nwalk - r0);
-      if (t < cn) {
-        const int a = a_lo + r0 + t;
+      if (tid < cn) {
+        const int a = a_lo + r0 + tid;
         int su;
         float nu[P + 1];
         if constexpr (P == 0) {
@@ -480,23 +476,38 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
             d_basis<P>(Uk, su, ua, P, nu);
           }
         }
-        su_s[t] = min(max(su, S0), S1 - 1);  // memory safety for inconsistent inputs
+        su_s[tid] = min(max(su, S0), S1 - 1);  // memory safety for inconsistent inputs
 #pragma unroll
-        for (int k = 0; k < NP; ++k) Nu_s[t * NP + k] = (k <= P) ? nu[k <= P ? k : 0] : 0.f;
+        for (int k = 0; k < NP; ++k) Nu_s[tid * NP + k] = (k <= P) ? nu[k <= P ? k : 0] : 0.f;
       }
-      bar_compute();
+      __syncthreads();
     }
     if constexpr (BULK) {
-      if (BWD) mbar_wait(full + slot, use & 1);
-      else if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
-      run_rows(ci0, nr, stage + slot * (kRPS * kCB * 3) + t * 3, (size_t)kCB * 3);
-      if constexpr (!BWD) fence_proxy_async();
-      mbar_arrive(BWD ? empty + slot : full + slot);
+      float* sslot = stage + slot * (RPS * SROW);
+      if constexpr (BWD) mbar_wait(sfull + slot, use & 1);
+      else if (use > 0) mbar_wait(sempty + slot, (use - 1) & 1);
+      run_rows(ci0, nr, sslot + tid * 3, SROW);
+      if constexpr (!BWD) fence_proxy_async();  // this thread's staged rows -> async proxy
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();  // release this warp's part of the stage
+        const int done = atomicAdd(scnt + slot, 1);
+        if (done == kThreads / 32 - 1) {  // last warp of this stage
+          scnt[slot] = 0;
+          __threadfence_block();  // acquire the other warps' parts
+          if constexpr (BWD) {
+            if (st + NST < nstage) issue_load(st + NST, slot);
+          } else {
+            issue_store(st, slot);
+          }
+        }
+      }
     } else {
       run_rows(ci0, nr, gio + (size_t)r0 * grow, grow);
     }
-    if (++slot == kStages) { slot = 0; ++use; }
+    if (++slot == NST) { slot = 0; ++use; }
   }
+  if constexpr (BULK && !BWD) bulk_wait_all();  // every store this thread issued has landed
 
   if constexpr (BWD) {
     // ---- B1 epilogue: flush the last window and the rows never reached (zeros), in order
@@ -505,12 +516,12 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 6) nurbs_grid_kernel(const
     for (int i = lo + P + 1; i < S1; ++i) flush_checked(i, f4(0.f));
     if (b2_next < S1) b2_batch(b2_next, S1 - b2_next);
 
-    if (!prm.direct && rb == 0 && t == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sfirst - Q, sfirst + nspan - 1);
+    if (!prm.direct && rb == 0 && tid == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sfirst - Q, sfirst + nspan - 1);
     if (prm.direct) {  // knot gradients are zero by definition
       if (prm.gR && s < prm.gR_items)
-        for (int x = t; x < prm.gR_per; x += kCompute) prm.gR[(size_t)s * prm.gR_per + x] = 0.f;
+        for (int x = tid; x < prm.gR_per; x += kThreads) prm.gR[(size_t)s * prm.gR_per + x] = 0.f;
       if (prm.gC && s < prm.gC_items)
-        for (int x = t; x < prm.gC_per; x += kCompute) prm.gC[(size_t)s * prm.gC_per + x] = 0.f;
+        for (int x = tid; x < prm.gC_per; x += kThreads) prm.gC[(size_t)s * prm.gC_per + x] = 0.f;
     }
   }
 }

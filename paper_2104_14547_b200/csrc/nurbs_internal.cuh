@@ -11,11 +11,13 @@
 
 namespace nb {
 
-constexpr int kCB = 128;          // sample columns per CTA block = compute threads
-constexpr int kCompute = 128;     // compute threads (4 warps)
-constexpr int kThreads = 160;     // + 1 producer warp issuing TMA bulk copies
-constexpr int kRPS = 8;           // sample rows per pipeline stage
-constexpr int kStages = 2;        // pipeline depth (stage ring)
+constexpr int kCB = 128;          // sample columns per CTA block = threads (one column each)
+constexpr int kCompute = 128;     // threads per CTA (4 warps)
+constexpr int kThreads = 128;
+constexpr int kRPS_F = 8;         // forward: sample rows per per-warp TMA stage
+constexpr int kStages_F = 2;      //          stages per warp ring
+constexpr int kRPS_B = 4;         // backward: sample rows per per-warp TMA stage
+constexpr int kStages_B = 4;      //           stages per warp ring (3 stages in flight)
 constexpr int kRowChunk = 64;     // rows whose span/basis are staged in smem at once
 constexpr int kMaxQ = 5;          // max column degree (runtime q)
 constexpr int kRMax = 16;         // max control rows in a row-block band
