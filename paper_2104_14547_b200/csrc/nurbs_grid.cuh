@@ -76,10 +76,9 @@ struct B2Args {
 };
 
 template <int Q>
-__device__ __forceinline__ void b2_batch_fn(const B2Args* __restrict__ ap, int i0, int nb) {
+__device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;
-  __syncthreads();        // H rows of the batch (and *ap) written by every thread
-  const B2Args a = *ap;  // CTA-uniform arguments live in smem, not in the walk's registers
+  __syncthreads();  // H rows of the batch written by every thread
   const int t = threadIdx.x, m = a.m;
   auto store_dq = [&](int i, int j, float4 a4) {
     if (a.direct) {  // dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
@@ -199,9 +198,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const
   float* Nv_s = reinterpret_cast<float*>(sv_s + kCB);                              // [kCB][NQ]  (bwd)
   int* sst = reinterpret_cast<int*>(Nv_s + kCB * NQ);                              // [kCB+4]    (bwd)
   int* misc = BWD ? sst + kCB + 4 : sv_s;                                          // [4]
-  B2Args* b2args = reinterpret_cast<B2Args*>(misc + 4);                           // (bwd)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(b2args) +
-                                               (BWD ? sizeof(B2Args) : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(misc + 4);                         // 8-byte aligned
   uint64_t* band_bar = bars;            // control band landed
   uint64_t* sfull = bars + 1;           // bwd: stage slot filled by TMA (count 1 + tx bytes)
   uint64_t* sempty = bars + 1 + NST;    // fwd: stage slot drained by TMA (count 1)
@@ -323,9 +320,8 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const
   mbar_wait(band_bar, 0);
   const int jlo = misc[0];
   const bool band_in_smem = misc[1] != 0;
-  const float4* crow0 = band_in_smem ? cband + (sv - Q - jlo) - (size_t)band_lo * prm.CBW
-                                     : ctrl_s + (sv - Q);
-  const int crow_stride = band_in_smem ? prm.CBW : m;
+  const float4* cb0 = cband + (sv - Q - jlo) - (size_t)band_lo * prm.CBW;  // smem band, row 0
+  const float4* cg0 = ctrl_s + (sv - Q);                                     // global, row 0
 
   // ---- backward: knot spans present in this column block. B2 runs one warp per control row
   // with one lane per span when the block touches at most 32 - q consecutive spans.
@@ -346,22 +342,23 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const
         sst[k] = lo2;
       }
     }
-    if (tid == 0) {
-      B2Args& b2a = *b2args;
-      b2a.Hring = Hring; b2a.Nv_s = Nv_s; b2a.sv_s = sv_s; b2a.sst = sst;
-      b2a.ctrl_s = ctrl_s; b2a.gctrl_s = prm.gctrl + (size_t)s * R.n * m;
-      b2a.slots = prm.slots ? prm.slots + (((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows * m : nullptr;
-      b2a.m = m; b2a.cols = cols; b2a.band_lo = band_lo; b2a.sfirst = sfirst; b2a.nspan = nspan;
-      b2a.fast = b2fast; b2a.direct = prm.direct;
-    }
+  }
+  B2Args b2a;
+  if constexpr (BWD) {
+    b2a.Hring = Hring; b2a.Nv_s = Nv_s; b2a.sv_s = sv_s; b2a.sst = sst;
+    b2a.ctrl_s = ctrl_s; b2a.gctrl_s = prm.gctrl + (size_t)s * R.n * m;
+    b2a.slots = prm.slots ? prm.slots + (((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows * m : nullptr;
+    b2a.m = m; b2a.cols = cols; b2a.band_lo = band_lo; b2a.sfirst = sfirst; b2a.nspan = nspan;
+    b2a.fast = b2fast; b2a.direct = prm.direct;
   }
   auto Trow = [&](int i) -> float4 {
-    const float4* src = crow0 + (size_t)i * crow_stride;
     float4 c[Q + 1];
     if (band_in_smem) {
+      const float4* src = cb0 + (size_t)i * prm.CBW;
 #pragma unroll
       for (int h = 0; h <= Q; ++h) c[h] = src[h];
     } else {
+      const float4* src = cg0 + (size_t)i * m;
 #pragma unroll
       for (int h = 0; h <= Q; ++h) c[h] = __ldg(src + h);
     }
@@ -372,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const
   };
 
   // ---- B2 (backward): batches of completed rows in the H ring -> dQ (b2_batch_fn)
-  auto b2_batch = [&](int i0, int nb) { b2_batch_fn<Q>(b2args, i0, nb); };
+  auto b2_batch = [&](int i0, int nb) { b2_batch_fn<Q>(b2a, i0, nb); };
   int b2_next = band_lo;  // first completed control row not yet reduced by B2
   // row i complete (uniform across the CTA): H(i) -> ring. The fast variant never reduces
   // (the stage loop guarantees ring capacity); the checked one reduces a full ring.
@@ -395,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const
     acc[k] = f4(0.f);
   }
 
+  const bool vio = BULK ? true : valid;  // TMA staging: columns >= cols use the unused row tail
   // One row of the walk: advance the window to the row's span if it changed (uniform across
   // the CTA, rare: once per knot span), then F2 (+ B1). ci = row index in the smem tables.
   auto row_step = [&](int ci, float* io, auto flush) {
@@ -420,15 +418,29 @@ __global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const
       const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
       nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
     }
-    walk_row<P, BWD>(nu, tw, acc, io, BULK && !BWD ? true : valid);
+    walk_row<P, BWD>(nu, tw, acc, io, vio);
   };
-  // rows [r0, r0+nr) of the walk: unrolled fast path when the H ring cannot overflow
+  // rows [r0, r0+nr) of the walk: unrolled fast paths when the window does not move (no span
+  // checks at all) or when the H ring cannot overflow
   auto run_rows = [&](int ci0, int nr, float* io0, size_t io_stride) {
-    bool fast = nr == RPS;
-    if constexpr (BWD) {  // rows completed by this stage = advance of the window
-      const int lo_end = max(lo, su_s[ci0 + nr - 1] - P);
-      fast = fast && (lo_end - b2_next) <= kHRing;
+    const int lo_end = max(lo, su_s[ci0 + nr - 1] - P);  // spans are non-decreasing
+    if (nr == RPS && lo_end == lo) {
+#pragma unroll
+      for (int r = 0; r < RPS; ++r) {
+        const float* nup = Nu_s + (ci0 + r) * NP;
+        float nu[NP];
+        const float4 n0 = *reinterpret_cast<const float4*>(nup);
+        nu[0] = n0.x; nu[1] = n0.y; nu[2] = n0.z; nu[3] = n0.w;
+        if constexpr (NP == 8) {
+          const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
+          nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
+        }
+        walk_row<P, BWD>(nu, tw, acc, io0 + r * io_stride, vio);
+      }
+      return;
     }
+    bool fast = nr == RPS;
+    if constexpr (BWD) fast = fast && (lo_end - b2_next) <= kHRing;  // ring capacity
     if (fast) {
 #pragma unroll
       for (int r = 0; r < RPS; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_fast);

@@ -14,15 +14,15 @@ namespace nb {
 constexpr int kCB = 128;          // sample columns per CTA block = threads (one column each)
 constexpr int kCompute = 128;     // threads per CTA (4 warps)
 constexpr int kThreads = 128;
-constexpr int kRPS_F = 8;         // forward: sample rows per per-warp TMA stage
-constexpr int kStages_F = 2;      //          stages per warp ring
-constexpr int kRPS_B = 4;         // backward: sample rows per per-warp TMA stage
-constexpr int kStages_B = 4;      //           stages per warp ring (3 stages in flight)
+constexpr int kRPS_F = 8;         // forward: sample rows per TMA stage
+constexpr int kStages_F = 2;      //          stages in the ring
+constexpr int kRPS_B = 8;         // backward: sample rows per TMA stage
+constexpr int kStages_B = 3;      //           stages in the ring (2 in flight)
 constexpr int kRowChunk = 64;     // rows whose span/basis are staged in smem at once
 constexpr int kMaxQ = 5;          // max column degree (runtime q)
 constexpr int kRMax = 16;         // max control rows in a row-block band
 constexpr int kBandCols = 32;     // smem capacity (columns) of the staged control band
-constexpr int kHRing = 8;         // completed-H rows buffered for B2 (power of 2)
+constexpr int kHRing = 4;         // completed-H rows buffered for B2 (power of 2)
 constexpr int kB2Batch = 4;       // B2 reduces completed rows in batches of this size
 constexpr int kTargetCTAs = 592;  // 4 resident CTAs x 148 SMs: planning target (fixed so the
                                   // plan, hence summation order, is a pure function of shape)

@@ -131,7 +131,6 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW) {
              (size_t)kRowChunk * NP * 4;
   if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4 + (kCB + 4) * 4;
   b += 4 * 4;                                  // misc
-  if (bwd) b += 128;                           // B2Args (see nurbs_grid.cuh)
   b = (b + 7) / 8 * 8 + (1 + 2 * nst) * 8 + nst * 4;  // mbarriers + stage counters
   return b;
 }
