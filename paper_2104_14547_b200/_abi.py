@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnurbs_b200.so")
+LIB_PATH = os.environ.get("NURBS_B200_LIB_EXPERIMENT") or os.path.join(HERE, "libnurbs_b200.so")
 
 NURBS_OK = 0
 NURBS_MAX_DEGREE = 5

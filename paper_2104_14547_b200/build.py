@@ -36,15 +36,16 @@ def deps():
     return glob.glob(os.path.join(CSRC, "*")) + [os.path.join(ROOT, "include", "nurbs.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in deps())
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()) -> str:
+    LIB_ = lib
+    stale = force or not os.path.exists(LIB_) or any(os.path.getmtime(d) > os.path.getmtime(LIB_) for d in deps())
     if not stale:
-        return LIB
+        return LIB_
     OBJ = tempfile.mkdtemp(prefix="nurbs_b200_obj_")
     procs = []
     for name, src, extra in units():
         obj = os.path.join(OBJ, name + ".o")
-        cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+        cmd = [NVCC] + FLAGS + list(defines) + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
         procs.append((name, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     objs, failed = [], False
     for name, obj, pr in procs:
@@ -57,13 +58,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     if failed:
         raise RuntimeError("nvcc failed building libnurbs_b200.so")
-    res = subprocess.run([NVCC] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs, capture_output=True, text=True)
+    res = subprocess.run([NVCC] + ARCH + ["-shared", "-o", LIB_ + ".tmp"] + objs, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(LIB_ + ".tmp", LIB_)
     shutil.rmtree(OBJ, ignore_errors=True)
-    return LIB
+    return LIB_
 
 
 if __name__ == "__main__":

@@ -158,7 +158,7 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
 }
 
 template <int P, int Q, bool BWD, bool BULK>
-__global__ void __launch_bounds__(kThreads, BWD ? 4 : 7) nurbs_grid_kernel(const Params prm) {
+__global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) nurbs_grid_kernel(const Params prm) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
@@ -561,6 +561,12 @@ static cudaError_t launch_pq(const Params& prm, bool bwd, cudaStream_t st) {
 
 template <int P>
 static cudaError_t launch_p(const Params& prm, bool bwd, int q, cudaStream_t st) {
+#ifdef NB_EXPERIMENT_PQ33  // tuning experiments: only the bicubic kernels
+  if constexpr (P == 3) {
+    if (q == 3) return launch_pq<3, 3>(prm, bwd, st);
+  }
+  return cudaErrorNotSupported;
+#else
   switch (q) {
     case 1: return launch_pq<P, 1>(prm, bwd, st);
     case 2: return launch_pq<P, 2>(prm, bwd, st);
@@ -569,6 +575,7 @@ static cudaError_t launch_p(const Params& prm, bool bwd, int q, cudaStream_t st)
     case 5: return launch_pq<P, 5>(prm, bwd, st);
     default: return cudaErrorInvalidValue;
   }
+#endif
 }
 
 }  // namespace nb

@@ -11,21 +11,55 @@
 
 namespace nb {
 
+// Tuning knobs (compile-time; -D overrides are for experiments only).
+#ifndef NB_RPS_F
+#define NB_RPS_F 8
+#endif
+#ifndef NB_STAGES_F
+#define NB_STAGES_F 2
+#endif
+#ifndef NB_RPS_B
+#define NB_RPS_B 8
+#endif
+#ifndef NB_STAGES_B
+#define NB_STAGES_B 3
+#endif
+#ifndef NB_HRING
+#define NB_HRING 4
+#endif
+#ifndef NB_B2BATCH
+#define NB_B2BATCH 4
+#endif
+#ifndef NB_ROWCHUNK
+#define NB_ROWCHUNK 64
+#endif
+#ifndef NB_MINB_F
+#define NB_MINB_F 7
+#endif
+#ifndef NB_MINB_B
+#define NB_MINB_B 4
+#endif
+#ifndef NB_TARGET_CTAS
+#define NB_TARGET_CTAS 2368
+#endif
+
 constexpr int kCB = 128;          // sample columns per CTA block = threads (one column each)
 constexpr int kCompute = 128;     // threads per CTA (4 warps)
 constexpr int kThreads = 128;
-constexpr int kRPS_F = 8;         // forward: sample rows per TMA stage
-constexpr int kStages_F = 2;      //          stages in the ring
-constexpr int kRPS_B = 8;         // backward: sample rows per TMA stage
-constexpr int kStages_B = 3;      //           stages in the ring (2 in flight)
-constexpr int kRowChunk = 64;     // rows whose span/basis are staged in smem at once
+constexpr int kRPS_F = NB_RPS_F;         // forward: sample rows per TMA stage
+constexpr int kStages_F = NB_STAGES_F;   //          stages in the ring
+constexpr int kRPS_B = NB_RPS_B;         // backward: sample rows per TMA stage
+constexpr int kStages_B = NB_STAGES_B;   //           stages in the ring (kStages_B-1 in flight)
+constexpr int kRowChunk = NB_ROWCHUNK;   // rows whose span/basis are staged in smem at once
 constexpr int kMaxQ = 5;          // max column degree (runtime q)
 constexpr int kRMax = 16;         // max control rows in a row-block band
 constexpr int kBandCols = 32;     // smem capacity (columns) of the staged control band
-constexpr int kHRing = 4;         // completed-H rows buffered for B2 (power of 2)
-constexpr int kB2Batch = 4;       // B2 reduces completed rows in batches of this size
-constexpr int kTargetCTAs = 592;  // 4 resident CTAs x 148 SMs: planning target (fixed so the
-                                  // plan, hence summation order, is a pure function of shape)
+constexpr int kHRing = NB_HRING;         // completed-H rows buffered for B2 (power of 2)
+constexpr int kB2Batch = NB_B2BATCH;     // B2 reduces completed rows in batches of this size
+constexpr int kMinBlocks_F = NB_MINB_F;  // __launch_bounds__ min CTAs per SM (register budget)
+constexpr int kMinBlocks_B = NB_MINB_B;
+constexpr int kTargetCTAs = NB_TARGET_CTAS;  // planning target (fixed so the plan, hence the
+                                             // summation order, is a pure function of shape)
 
 // One parametric direction.
 struct Dir {
