@@ -33,7 +33,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=4, choices=[4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="oracle cpu_baseline time budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -196,9 +196,111 @@ def run_reference(args, rank, world):
 
 
 def workload_name(config):
+    if config == 3:
+        return ("cfg3: SGD surface fit, 1 bicubic NURBS 32x32 control net, 512x512 target grid, "
+                "one fused fwd+MSE+bwd+update step per iteration, iterations in one CUDA graph (configs[2])")
     if config == 4:
         return "cfg4: 4096 bicubic NURBS surfaces x 16x16 control nets, 128x128 grid each, fwd+bwd (BASELINE.json configs[3])"
     return "cfg5: one bicubic 256x256 NURBS surface, 8192x8192 grid, u-rows sharded, fwd+bwd+allreduce (configs[4])"
+
+
+# --------------------------------------------------------------------------- config 3: fitting loop
+def run_fit(args, rank, world):
+    """Config 3: K SGD iterations of the fused fitting step, recorded in one
+    CUDA graph and replayed; inputs resident in HBM (the 3 MB target stays L2-resident across
+    iterations, so this loop is latency-bound, not HBM-bound)."""
+    import numpy as np
+    import torch
+
+    import paper_2104_14547_b200 as nb
+    import workloads as wl
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    truth, init = wl.config3_fit()
+    T_ = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    U, V, u, v = T_(truth.U), T_(truth.V), T_(truth.u), T_(truth.v)
+    sh = nb.nurbs_shape(1, 32, 32, 3, 3, 512, 512, 0)
+    tables = nb.Tables.build(sh, U, V, u, v)
+    target = nb.surface_fwd(T_(truth.ctrl), U, V, u, v, 3, 3, tables=tables)  # synthetic target
+    ctrl = T_(init.ctrl)
+    fitter = nb.SurfaceFitter(ctrl, U, V, u, v, target, 3, 3, lr=200.0, tables=tables)
+    K = args.steps
+    fitter.run(K)            # warm-up: records the graph and runs it once
+    for _ in range(max(0, args.warmup - 1)):
+        fitter.run(K)
+    ctrl.copy_(T_(init.ctrl))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        e0.record()
+        losses = fitter.run(K)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    lh = losses.cpu().numpy()
+    pts = 512 * 512
+    # one un-graphed iteration through the C ABI with host buffers (e2e)
+    h_ctrl = init.ctrl.copy()
+    h_target = target.cpu().pin_memory()
+    E = 20
+    d_ctrl, d_t = torch.empty_like(ctrl), torch.empty_like(target)
+    h_out = torch.empty(ctrl.shape, dtype=torch.float32).pin_memory()
+    h_loss = torch.empty(1, dtype=torch.float32).pin_memory()
+    lossd = torch.zeros(1, device=dev)
+    f2 = nb.SurfaceFitter(d_ctrl, U, V, u, v, d_t, 3, 3, lr=200.0, tables=tables)
+    h_c = torch.from_numpy(h_ctrl).pin_memory()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(E):
+        d_ctrl.copy_(h_c, non_blocking=True)
+        d_t.copy_(h_target, non_blocking=True)
+        f2.step(lossd)
+        h_out.copy_(d_ctrl, non_blocking=True)
+        h_loss.copy_(lossd, non_blocking=True)
+    e3.record()
+    torch.cuda.synchronize()
+    e2e_ms = e2.elapsed_time(e3) / E
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        c = init.ctrl.astype(np.float64)
+        Tt = target.cpu().numpy().astype(np.float64)
+        t0 = time.perf_counter()
+        it = 0
+        while time.perf_counter() - t0 < args.cpu_seconds and it < 200:
+            S = oracle.surface_fwd(c, truth.U, truth.V, truth.u, truth.v, 3, 3)
+            d = S - Tt
+            g = oracle.surface_bwd(c, truth.U, truth.V, truth.u, truth.v, 2 * d / pts, 3, 3)
+            c = c - 200.0 * g
+            it += 1
+        dt = time.perf_counter() - t0
+        cpu = {"value": pts * it / dt, "unit": "points/s", "cores": 1, "kind": "oracle",
+               "sample": f"cfg3: {it} fitting iterations (fwd+MSE+bwd+SGD) at 512x512, fp64, 1 thread",
+               "it_per_s": it / dt}
+    line = {
+        "metric": METRIC, "value": pts * K / (ms * 1e-3), "unit": "points/s", "n_gpus": 1, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "replicas only",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded ground-truth NURBS target; init P*+N(0,0.05), w=1)",
+        "config": {"workload": workload_name(3), "lr": 200.0, "iterations_timed": K,
+                   "l2": "target (3 MB) L2-resident across iterations by design of the loop"},
+        "it_per_s": K / (ms * 1e-3),
+        "loss_first_last": [float(lh[0]), float(lh[-1])],
+        "paper_context": "Ducky fit, 14x13 net at 512^2: 1000 iterations in < 2 minutes (>= 8.3 it/s), hardware unstated (P:480)",
+        "roofline": {"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
+                     "note": "2 launches per iteration (fused step + update) on a 262K-point problem"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": pts / (e2e_ms * 1e-3), "unit": "points/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": init.ctrl.nbytes + target.numel() * 4,
+                "d2h_bytes_per_step": init.ctrl.nbytes + 4},
+        "gpu_launches": 2 * K,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------- our arm
@@ -209,6 +311,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.config == 3:
+        return run_fit(args, rank, world)
 
     import torch
     import torch.distributed as dist

@@ -114,6 +114,24 @@ int    nurbs_surface_bwd(const nurbs_shape* shape, const float* ctrl,
 size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* shape);
 
 /* ---------------------------------------------------------------------------------------
+ * Fused fitting step (the surface-fitting loop of §4.2, with Eq.14):
+ * one SGD iteration of  L = mean over the n_u x n_v x B points of |S - T|^2  (R20) with
+ * respect to the control points and weights, in place:
+ *     S = f(ctrl) (Eq.3);  loss = L;  dL/dS = 2 (S - T) / N;  grad_ctrl = J^T dL/dS (Eq.8/9);
+ *     ctrl <- ctrl - lr * grad_ctrl   (x, y, z and w; knots fixed).
+ * target [B][n_u][n_v][3]; ctrl [B][n][m][4] is read and updated; grad_ctrl [B][n][m][4]
+ * receives the gradient at the pre-update ctrl; loss is a DEVICE float receiving L at the
+ * pre-update ctrl. S is never written to HBM (the forward and backward are one kernel).
+ * Workspace: nurbs_surface_fit_workspace_bytes(shape) bytes (never 0). Deterministic.
+ * --------------------------------------------------------------------------------------- */
+int    nurbs_surface_fit_step(const nurbs_shape* shape, float* ctrl,
+                              const float* U, const float* V, const float* u, const float* v,
+                              const void* tables, const float* target, float lr,
+                              float* grad_ctrl, float* loss,
+                              void* workspace, size_t ws_bytes, void* stream);
+size_t nurbs_surface_fit_workspace_bytes(const nurbs_shape* shape);
+
+/* ---------------------------------------------------------------------------------------
  * Curves: shape.m = 1, shape.q = 0. Same semantics as the surface calls.
  * --------------------------------------------------------------------------------------- */
 int    nurbs_curve_fwd(const nurbs_shape* shape, const float* ctrl, const float* U,

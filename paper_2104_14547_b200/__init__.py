@@ -21,4 +21,7 @@ from .api import (  # noqa: F401
     surface_shape,
     curve_shape,
     bwd_workspace_bytes,
+    fit_workspace_bytes,
+    nurbs_surface_fit_step,
+    SurfaceFitter,
 )

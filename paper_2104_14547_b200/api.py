@@ -96,6 +96,18 @@ def nurbs_curve_bwd(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspa
                                  ctypes.c_size_t(ws_bytes), _stream(stream)), "nurbs_curve_bwd")
 
 
+def nurbs_surface_fit_step(sh, ctrl, U, V, u, v, tables, target, lr, grad_ctrl, loss, workspace, ws_bytes,
+                           stream=None):
+    check(load().nurbs_surface_fit_step(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
+                                        _ptr(tables), _ptr(target), ctypes.c_float(lr), _ptr(grad_ctrl),
+                                        _ptr(loss), _ptr(workspace), ctypes.c_size_t(ws_bytes), _stream(stream)),
+          "nurbs_surface_fit_step")
+
+
+def fit_workspace_bytes(sh: nurbs_shape) -> int:
+    return int(load().nurbs_surface_fit_workspace_bytes(ctypes.byref(sh)))
+
+
 def nurbs_validate(sh, ctrl, U, V, u, v, stream=None):
     check(load().nurbs_validate(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
                                 _stream(stream)), "nurbs_validate")
@@ -156,3 +168,45 @@ def curve_bwd(ctrl, U, u, grad_out, p: int, tables: Tables | None = None, grad_c
         workspace = torch.empty(ws, dtype=torch.uint8, device=ctrl.device)
     nurbs_curve_bwd(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspace, ws, stream)
     return grad_ctrl
+
+
+class SurfaceFitter:
+    """The fitting loop of §4.2: SGD on P and w of one batch of surfaces toward a
+    target point grid, each iteration one fused step (nurbs_surface_fit_step). `run(iters)`
+    records `iters` steps once into a CUDA graph (no host work per iteration) and replays it.
+    Argument marshalling only: every iteration runs in libnurbs_b200's kernels."""
+
+    def __init__(self, ctrl, U, V, u, v, target, p: int, q: int, lr: float, tables: "Tables | None" = None):
+        self.ctrl, self.U, self.V, self.u, self.v, self.target = ctrl, U, V, u, v, target
+        self.sh = surface_shape(ctrl, U, u, v, p, q)
+        self.lr, self.tables = lr, tables
+        self.grad = torch.empty_like(ctrl)
+        self.ws_bytes = fit_workspace_bytes(self.sh)
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=ctrl.device)
+        self.losses = None
+        self._graph = None
+
+    def step(self, loss_out, stream=None):
+        nurbs_surface_fit_step(self.sh, self.ctrl, self.U, self.V, self.u, self.v, self.tables, self.target,
+                               self.lr, self.grad, loss_out, self.ws, self.ws_bytes, stream)
+
+    def run(self, iters: int, graph: bool = True) -> torch.Tensor:
+        """Run `iters` steps; returns the per-iteration loss history (device tensor)."""
+        if self.losses is None or self.losses.numel() != iters:
+            self.losses = torch.zeros(iters, dtype=torch.float32, device=self.ctrl.device)
+            self._graph = None
+        if not graph:
+            for k in range(iters):
+                self.step(self.losses[k:k + 1])
+            return self.losses
+        if self._graph is None:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for k in range(iters):
+                    self.step(self.losses[k:k + 1], stream=s)
+            torch.cuda.current_stream().wait_stream(s)
+            self._graph = g
+        self._graph.replay()
+        return self.losses

@@ -177,12 +177,59 @@ int launch(const Geo& g, bool bwd, const float* ctrl, float* out, const float* g
     prm.slots = reinterpret_cast<float4*>(ws);
     prm.colband = reinterpret_cast<int2*>(static_cast<unsigned char*>(ws) + pl.slots_bytes);
   }
-  cudaError_t e = nb::launch_grid(prm, bwd, g.P, g.c.p, st);
+  cudaError_t e = nb::launch_grid(prm, bwd ? 1 : 0, g.P, g.c.p, st);
   if (e != cudaSuccess) return cuda_fail(e, bwd ? "backward kernel launch" : "forward kernel launch");
   if (bwd && !pl.direct) {
     e = nb::launch_reduce(prm, g.P, st);
     if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
   }
+  return NURBS_OK;
+}
+
+// Fused fitting step (NEXT-2): grid kernel with dL/dS = 2 (S - T) / N from the target, then
+// the update kernel (tile reduce if needed, SGD on P and w, loss).
+int launch_fit(const Geo& g, float* ctrl, const float* target, float lr, float* gctrl, float* loss, void* ws,
+               size_t ws_bytes, cudaStream_t st) {
+  const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns);
+  if (g.B == 0) return NURBS_OK;
+  if (g.r.ns == 0 || g.c.ns == 0) {
+    cudaError_t e = cudaMemsetAsync(gctrl, 0, (size_t)g.B * g.r.n * g.c.n * 16, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(loss, 0, sizeof(float), st);
+    return e == cudaSuccess ? NURBS_OK : cuda_fail(e, "zero-fill");
+  }
+  if (pl.grid > 0x7fffffffLL) return fail(NURBS_E_ARG, "grid of %lld CTAs too large", pl.grid);
+  if (!ws || ws_bytes < pl.fit_ws_bytes)
+    return fail(NURBS_E_WORKSPACE, "fit step needs a %zu-byte workspace (got %zu at %p)", pl.fit_ws_bytes, ws_bytes, ws);
+  Params prm{};
+  prm.B = g.B;
+  prm.r = g.r;
+  prm.c = g.c;
+  prm.ctrl = reinterpret_cast<const float4*>(ctrl);
+  prm.gout = target;
+  prm.gctrl = reinterpret_cast<float4*>(gctrl);
+  prm.K = pl.K;
+  prm.NRB = pl.NRB;
+  prm.NCB = pl.NCB;
+  prm.T_rows = pl.T_rows;
+  prm.CBW = g.c.n < nb::kBandCols ? g.c.n : nb::kBandCols;
+  prm.direct = pl.direct;
+  prm.bulk = (g.c.ns % 4 == 0) && aligned16(target) ? 1 : 0;
+  if (getenv("NURBS_NO_TMA")) prm.bulk = 0;
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  if (!pl.direct) {
+    prm.slots = reinterpret_cast<float4*>(w);
+    prm.colband = reinterpret_cast<int2*>(w + pl.slots_bytes);
+  }
+  prm.loss_parts = reinterpret_cast<float*>(w + pl.ws_bytes);
+  prm.n_parts = (int)pl.grid;
+  prm.loss = loss;
+  prm.ctrl_mut = reinterpret_cast<float4*>(ctrl);
+  prm.lr = lr;
+  prm.fit_scale = (float)(2.0 / ((double)g.B * g.r.ns * g.c.ns));
+  cudaError_t e = nb::launch_grid(prm, 2, g.P, g.c.p, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fit kernel launch");
+  e = nb::launch_fit_update(prm, g.P, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fit update kernel launch");
   return NURBS_OK;
 }
 
@@ -263,6 +310,29 @@ int nurbs_tables(const nurbs_shape* sh, const float* U, const float* V, const fl
 size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* sh) {
   if (!sh || sh->B <= 0) return 0;
   return nb::make_plan(sh->B, sh->n, sh->p, sh->n_u, sh->m, sh->n_v).ws_bytes;
+}
+
+size_t nurbs_surface_fit_workspace_bytes(const nurbs_shape* sh) {
+  if (!sh || sh->B <= 0) return 0;
+  return nb::make_plan(sh->B, sh->n, sh->p, sh->n_u, sh->m, sh->n_v).fit_ws_bytes;
+}
+
+int nurbs_surface_fit_step(const nurbs_shape* sh, float* ctrl, const float* U, const float* V, const float* u,
+                           const float* v, const void* tables, const float* target, float lr, float* grad_ctrl,
+                           float* loss, void* workspace, size_t ws_bytes, void* stream) {
+  g_detail.clear();
+  int st = check_surface_shape(sh);
+  if (st) return st;
+  if (sh->B == 0) return NURBS_OK;
+  if (!grad_ctrl || !loss) return fail(NURBS_E_ARG, "grad_ctrl and loss must not be NULL");
+  if (sh->n_u > 0 && sh->n_v > 0 && (st = check_ptrs(true, ctrl, nullptr, target, grad_ctrl))) return st;
+  if (!tables && (!U || !V || !u || !v)) return fail(NURBS_E_ARG, "NULL knots or samples");
+  if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = surface_geo(sh, U, V, u, v);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  attach_tables(g, tables);
+  return launch_fit(g, ctrl, target, lr, grad_ctrl, loss, workspace, ws_bytes, s);
 }
 
 size_t nurbs_curve_bwd_workspace_bytes(const nurbs_shape* sh) {

@@ -31,9 +31,10 @@ namespace nb {
 // One row of the walk (F2, and B1 in the backward) for one column: uniform across the CTA
 // except for the column data. `nu` = basis of the row, `tw` = the T window (P+1 control rows
 // [lo, lo+P] of this column), `io` = this thread's 3 floats of the output / dL/dS row.
-template <int P, bool BWD>
+template <int P, bool BWD, bool FIT>
 __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const float4 (&tw)[P + 1],
-                                         float4 (&acc)[P + 1], float* io, bool valid) {
+                                         float4 (&acc)[P + 1], float* io, bool valid, float fit_scale,
+                                         float& lsum) {
   float4 Sp = f4(0.f);
 #pragma unroll
   for (int k = 0; k <= P; ++k) Sp = fma4v(nu[k], tw[k], Sp);
@@ -46,9 +47,24 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
       io[2] = Sp.z * rw;
     }
   } else {
-    const float gx = valid ? io[0] : 0.f;
-    const float gy = valid ? io[1] : 0.f;
-    const float gz = valid ? io[2] : 0.f;
+    float gx, gy, gz;
+    if constexpr (FIT) {
+      // fused fitting step (NEXT-2): io holds the target T; L = mean |S - T|^2 over the
+      // points, so g = dL/dS = fit_scale * (S - T) with fit_scale = 2 / (number of points)
+      const float2 sxy = up2(fmul2(pk2(Sp.x, Sp.y), pk2(rw, rw)));
+      const float sz = Sp.z * rw;
+      const float dx = valid ? sxy.x - io[0] : 0.f;
+      const float dy = valid ? sxy.y - io[1] : 0.f;
+      const float dz = valid ? sz - io[2] : 0.f;
+      lsum = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, lsum)));
+      gx = fit_scale * dx;
+      gy = fit_scale * dy;
+      gz = fit_scale * dz;
+    } else {
+      gx = valid ? io[0] : 0.f;
+      gy = valid ? io[1] : 0.f;
+      gz = valid ? io[2] : 0.f;
+    }
     // G = (g/W, -(g.S)/W) with S = S'_xyz / W  (Eq.8/9 through the homogeneous point)
     const float2 gxy = up2(fmul2(pk2(gx, gy), pk2(rw, rw)));
     const float gzr = gz * rw;
@@ -157,8 +173,9 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
   __syncthreads();  // ring slots free again
 }
 
-template <int P, int Q, bool BWD, bool BULK>
+template <int P, int Q, bool BWD, bool BULK, bool FIT>
 __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) nurbs_grid_kernel(const Params prm) {
+  static_assert(!FIT || BWD, "the fitting step is a backward variant");
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
@@ -392,7 +409,10 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     acc[k] = f4(0.f);
   }
 
-  const bool vio = BULK ? true : valid;  // TMA staging: columns >= cols use the unused row tail
+  // TMA staging: columns >= cols use the unused row tail (the fit step still masks its loss)
+  const bool vio = (BULK && !FIT) ? true : valid;
+  const float fit_scale = prm.fit_scale;
+  float lsum = 0.f;  // FIT: this thread's sum of |S - T|^2
   // One row of the walk: advance the window to the row's span if it changed (uniform across
   // the CTA, rare: once per knot span), then F2 (+ B1). ci = row index in the smem tables.
   auto row_step = [&](int ci, float* io, auto flush) {
@@ -418,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
       const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
       nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
     }
-    walk_row<P, BWD>(nu, tw, acc, io, vio);
+    walk_row<P, BWD, FIT>(nu, tw, acc, io, vio, fit_scale, lsum);
   };
   // rows [r0, r0+nr) of the walk: unrolled fast paths when the window does not move (no span
   // checks at all) or when the H ring cannot overflow
@@ -435,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
           const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
           nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
         }
-        walk_row<P, BWD>(nu, tw, acc, io0 + r * io_stride, vio);
+        walk_row<P, BWD, FIT>(nu, tw, acc, io0 + r * io_stride, vio, fit_scale, lsum);
       }
       return;
     }
@@ -528,6 +548,15 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     for (int i = lo + P + 1; i < S1; ++i) flush_checked(i, f4(0.f));
     if (b2_next < S1) b2_batch(b2_next, S1 - b2_next);
 
+    if constexpr (FIT) {  // per-CTA loss partial, fixed-order reduction
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+      float* lw = reinterpret_cast<float*>(su_s);  // the row tables are free now
+      __syncthreads();
+      if (lane == 0) lw[warp] = lsum;
+      __syncthreads();
+      if (tid == 0) prm.loss_parts[blockIdx.x] = (lw[0] + lw[1]) + (lw[2] + lw[3]);
+    }
     if (!prm.direct && rb == 0 && tid == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sfirst - Q, sfirst + nspan - 1);
     if (prm.direct) {  // knot gradients are zero by definition
       if (prm.gR && s < prm.gR_items)
@@ -538,41 +567,43 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   }
 }
 
-template <int P, int Q, bool BWD, bool BULK>
+template <int P, int Q, bool BWD, bool BULK, bool FIT>
 static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
   const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows, prm.CBW);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, BULK>,
+    cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, BULK, FIT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  nurbs_grid_kernel<P, Q, BWD, BULK>
+  nurbs_grid_kernel<P, Q, BWD, BULK, FIT>
       <<<(unsigned)((long long)prm.B * prm.NRB * prm.NCB), kThreads, smem, st>>>(prm);
   return cudaGetLastError();
 }
 
+// mode: 0 forward, 1 backward, 2 fused fitting step (backward with dL/dS from a target)
 template <int P, int Q>
-static cudaError_t launch_pq(const Params& prm, bool bwd, cudaStream_t st) {
-  if (bwd) return prm.bulk ? launch_one<P, Q, true, true>(prm, st) : launch_one<P, Q, true, false>(prm, st);
-  return prm.bulk ? launch_one<P, Q, false, true>(prm, st) : launch_one<P, Q, false, false>(prm, st);
+static cudaError_t launch_pq(const Params& prm, int mode, cudaStream_t st) {
+  if (mode == 2) return prm.bulk ? launch_one<P, Q, true, true, true>(prm, st) : launch_one<P, Q, true, false, true>(prm, st);
+  if (mode == 1) return prm.bulk ? launch_one<P, Q, true, true, false>(prm, st) : launch_one<P, Q, true, false, false>(prm, st);
+  return prm.bulk ? launch_one<P, Q, false, true, false>(prm, st) : launch_one<P, Q, false, false, false>(prm, st);
 }
 
 template <int P>
-static cudaError_t launch_p(const Params& prm, bool bwd, int q, cudaStream_t st) {
+static cudaError_t launch_p(const Params& prm, int mode, int q, cudaStream_t st) {
 #ifdef NB_EXPERIMENT_PQ33  // tuning experiments: only the bicubic kernels
   if constexpr (P == 3) {
-    if (q == 3) return launch_pq<3, 3>(prm, bwd, st);
+    if (q == 3) return launch_pq<3, 3>(prm, mode, st);
   }
   return cudaErrorNotSupported;
 #else
   switch (q) {
-    case 1: return launch_pq<P, 1>(prm, bwd, st);
-    case 2: return launch_pq<P, 2>(prm, bwd, st);
-    case 3: return launch_pq<P, 3>(prm, bwd, st);
-    case 4: return launch_pq<P, 4>(prm, bwd, st);
-    case 5: return launch_pq<P, 5>(prm, bwd, st);
+    case 1: return launch_pq<P, 1>(prm, mode, st);
+    case 2: return launch_pq<P, 2>(prm, mode, st);
+    case 3: return launch_pq<P, 3>(prm, mode, st);
+    case 4: return launch_pq<P, 4>(prm, mode, st);
+    case 5: return launch_pq<P, 5>(prm, mode, st);
     default: return cudaErrorInvalidValue;
   }
 #endif

@@ -9,7 +9,7 @@
 namespace nb {
 #define NB_CAT2(a, b) a##b
 #define NB_CAT(a, b) NB_CAT2(a, b)
-cudaError_t NB_CAT(launch_grid_p, NB_P)(const Params& prm, bool bwd, int q, cudaStream_t st) {
-  return launch_p<NB_P>(prm, bwd, q, st);
+cudaError_t NB_CAT(launch_grid_p, NB_P)(const Params& prm, int mode, int q, cudaStream_t st) {
+  return launch_p<NB_P>(prm, mode, q, st);
 }
 }  // namespace nb

@@ -91,6 +91,13 @@ struct Params {
   int direct;               // 1: bwd writes grad_ctrl in-kernel (NRB == NCB == 1)
   float4* slots;            // [B][NRB][NCB][T_rows][c.n] partial dQ (direct == 0)
   int2* colband;            // [B][NCB] (j0, j1) column band of each column block
+  // fused fitting step (NEXT-2)
+  float fit_scale;          // 2 / (number of points): dL/dS = fit_scale (S - T)
+  float* loss_parts;        // [grid] per-CTA sum of |S - T|^2
+  float* loss;              // device scalar: mean |S - T|^2
+  float4* ctrl_mut;         // ctrl updated in place: P -= lr dL/dP, w -= lr dL/dw (Eq.14)
+  float lr;
+  int n_parts;
 };
 
 // Tables blob layout (nurbs_tables): header then four arrays, each 256-byte aligned.
@@ -122,6 +129,7 @@ struct Plan {
   int K, NRB, NCB, T_rows, direct;
   long long grid;
   size_t slots_bytes, colband_bytes, ws_bytes;
+  size_t fit_ws_bytes;      // workspace of the fused fitting step (adds the loss partials)
 };
 
 inline Plan make_plan(int B, int n_r, int P, int ns_r, int n_c, int ns_c) {
@@ -144,13 +152,16 @@ inline Plan make_plan(int B, int n_r, int P, int ns_r, int n_c, int ns_c) {
     pl.colband_bytes = align_up((size_t)B * pl.NCB * sizeof(int2), 256);
     pl.ws_bytes = pl.slots_bytes + pl.colband_bytes;
   }
+  pl.fit_ws_bytes = pl.ws_bytes + align_up((size_t)(pl.grid > 0 ? pl.grid : 1) * sizeof(float), 256);
   (void)ns_r;
   return pl;
 }
 
 // Launchers (nurbs_kernels.cu). Return cudaError_t of the launch.
-cudaError_t launch_grid(const Params& prm, bool bwd, int P, int q, cudaStream_t st);
+cudaError_t launch_grid(const Params& prm, int mode, int P, int q, cudaStream_t st);  // mode 0 fwd, 1 bwd, 2 fit
 cudaError_t launch_reduce(const Params& prm, int P, cudaStream_t st);
+// fitting step: (reduce tile partials if needed) + SGD update of ctrl + loss = sum of the CTA partials
+cudaError_t launch_fit_update(const Params& prm, int P, cudaStream_t st);
 cudaError_t launch_tables(const Dir& r, const Dir& c, void* tables, const TabLayout& L,
                           cudaStream_t st);
 // status: device buffer of one unsigned long long, pre-set to ~0ull.
@@ -162,10 +173,10 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW);
 }  // namespace nb
 
 namespace nb {
-cudaError_t launch_grid_p0(const Params& prm, bool bwd, int q, cudaStream_t st);
-cudaError_t launch_grid_p1(const Params& prm, bool bwd, int q, cudaStream_t st);
-cudaError_t launch_grid_p2(const Params& prm, bool bwd, int q, cudaStream_t st);
-cudaError_t launch_grid_p3(const Params& prm, bool bwd, int q, cudaStream_t st);
-cudaError_t launch_grid_p4(const Params& prm, bool bwd, int q, cudaStream_t st);
-cudaError_t launch_grid_p5(const Params& prm, bool bwd, int q, cudaStream_t st);
+cudaError_t launch_grid_p0(const Params& prm, int mode, int q, cudaStream_t st);
+cudaError_t launch_grid_p1(const Params& prm, int mode, int q, cudaStream_t st);
+cudaError_t launch_grid_p2(const Params& prm, int mode, int q, cudaStream_t st);
+cudaError_t launch_grid_p3(const Params& prm, int mode, int q, cudaStream_t st);
+cudaError_t launch_grid_p4(const Params& prm, int mode, int q, cudaStream_t st);
+cudaError_t launch_grid_p5(const Params& prm, int mode, int q, cudaStream_t st);
 }  // namespace nb

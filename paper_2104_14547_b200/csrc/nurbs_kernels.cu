@@ -12,6 +12,7 @@ namespace nb {
 // ------------------------------------------------------------------------ cross-tile reduce
 // dQ_ij = sum over row blocks rb (ascending) and column blocks cb (ascending) whose bands
 // contain (i, j) of the tile partials; then the Eq.8/9 epilogue. One thread per control point.
+template <bool FIT>
 __global__ void __launch_bounds__(256) nurbs_reduce_kernel(const Params prm, int P) {
   const long long total = (long long)prm.B * prm.r.n * prm.c.n;
   const long long gsz = (long long)gridDim.x * blockDim.x;
@@ -20,33 +21,49 @@ __global__ void __launch_bounds__(256) nurbs_reduce_kernel(const Params prm, int
     for (long long x = idx0; x < (long long)prm.gR_items * prm.gR_per; x += gsz) prm.gR[x] = 0.f;
   if (prm.gC)
     for (long long x = idx0; x < (long long)prm.gC_items * prm.gC_per; x += gsz) prm.gC[x] = 0.f;
+  if (FIT && blockIdx.x == 0 && threadIdx.x < 32) {  // loss = mean |S - T|^2, fixed order
+    float a = 0.f;
+    for (int x = threadIdx.x; x < prm.n_parts; x += 32) a += prm.loss_parts[x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (threadIdx.x == 0) *prm.loss = a * (0.5f * prm.fit_scale);
+  }
   for (long long idx = idx0; idx < total; idx += gsz) {
-    const int m = prm.c.n;
-    const int j = (int)(idx % m);
-    const long long t2 = idx / m;
-    const int i = (int)(t2 % prm.r.n);
-    const int s = (int)(t2 / prm.r.n);
-    const int K = prm.K;
-    const int rb_hi = min(prm.NRB - 1, i / K);
-    const int x = i - K - P + 1;
-    const int rb_lo = x <= 0 ? 0 : (x + K - 1) / K;
-    const int2* cbands = prm.colband + (size_t)s * prm.NCB;
-    int lo = 0, hi = prm.NCB;  // first cb with j1 >= j
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (cbands[mid].y < j) lo = mid + 1; else hi = mid;
-    }
-    float4 a4 = f4(0.f);
-    for (int rb = rb_lo; rb <= rb_hi; ++rb) {
-      const int r = i - rb * K;
-      for (int cb = lo; cb < prm.NCB && cbands[cb].x <= j; ++cb) {
-        const float4 v = prm.slots[((((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows + r) * m + j];
-        a4.x += v.x; a4.y += v.y; a4.z += v.z; a4.w += v.w;
-      }
-    }
     const float4 c = __ldg(prm.ctrl + idx);
-    prm.gctrl[idx] =
-        make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
+    float4 g;
+    if (FIT && prm.direct) {
+      g = prm.gctrl[idx];  // written by the grid kernel's epilogue
+    } else {
+      const int m = prm.c.n;
+      const int j = (int)(idx % m);
+      const long long t2 = idx / m;
+      const int i = (int)(t2 % prm.r.n);
+      const int s = (int)(t2 / prm.r.n);
+      const int K = prm.K;
+      const int rb_hi = min(prm.NRB - 1, i / K);
+      const int x = i - K - P + 1;
+      const int rb_lo = x <= 0 ? 0 : (x + K - 1) / K;
+      const int2* cbands = prm.colband + (size_t)s * prm.NCB;
+      int lo = 0, hi = prm.NCB;  // first cb with j1 >= j
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cbands[mid].y < j) lo = mid + 1; else hi = mid;
+      }
+      float4 a4 = f4(0.f);
+      for (int rb = rb_lo; rb <= rb_hi; ++rb) {
+        const int r = i - rb * K;
+        for (int cb = lo; cb < prm.NCB && cbands[cb].x <= j; ++cb) {
+          const float4 v = prm.slots[((((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows + r) * m + j];
+          a4.x += v.x; a4.y += v.y; a4.z += v.z; a4.w += v.w;
+        }
+      }
+      // epilogue (Eq.8/9): dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
+      g = make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
+      if (prm.gctrl) prm.gctrl[idx] = g;
+    }
+    if (FIT)  // SGD step (Eq.14): Psi <- Psi - lr dL/dPsi on P and w
+      prm.ctrl_mut[idx] = make_float4(fmaf(-prm.lr, g.x, c.x), fmaf(-prm.lr, g.y, c.y), fmaf(-prm.lr, g.z, c.z),
+                                      fmaf(-prm.lr, g.w, c.w));
   }
 }
 
@@ -135,14 +152,14 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW) {
   return b;
 }
 
-cudaError_t launch_grid(const Params& prm, bool bwd, int P, int q, cudaStream_t st) {
+cudaError_t launch_grid(const Params& prm, int mode, int P, int q, cudaStream_t st) {
   switch (P) {
-    case 0: return launch_grid_p0(prm, bwd, q, st);
-    case 1: return launch_grid_p1(prm, bwd, q, st);
-    case 2: return launch_grid_p2(prm, bwd, q, st);
-    case 3: return launch_grid_p3(prm, bwd, q, st);
-    case 4: return launch_grid_p4(prm, bwd, q, st);
-    case 5: return launch_grid_p5(prm, bwd, q, st);
+    case 0: return launch_grid_p0(prm, mode, q, st);
+    case 1: return launch_grid_p1(prm, mode, q, st);
+    case 2: return launch_grid_p2(prm, mode, q, st);
+    case 3: return launch_grid_p3(prm, mode, q, st);
+    case 4: return launch_grid_p4(prm, mode, q, st);
+    case 5: return launch_grid_p5(prm, mode, q, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -152,7 +169,16 @@ cudaError_t launch_reduce(const Params& prm, int P, cudaStream_t st) {
   long long blocks = (total + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  nurbs_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(prm, P);
+  nurbs_reduce_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(prm, P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fit_update(const Params& prm, int P, cudaStream_t st) {
+  const long long total = (long long)prm.B * prm.r.n * prm.c.n;
+  long long blocks = (total + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  nurbs_reduce_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(prm, P);
   return cudaGetLastError();
 }
 

@@ -352,3 +352,63 @@ def test_config5_full_size_sampled():
     lhs = grad[0, ..., :3].astype(np.float64).sum(axis=(0, 1))
     rhs = g[0].astype(np.float64).sum(axis=(0, 1))
     assert np.max(np.abs(lhs - rhs)) / np.abs(g).astype(np.float64).sum() <= 1e-5
+
+
+# --------------------------------------------------------------------------- fused fitting step (NEXT-2)
+def oracle_fit(ctrl0, w, T, lr, iters):
+    """fp64 oracle loop of the fitting step: L = mean |S - T|^2, SGD on P and w (Eq.14)."""
+    c = ctrl0.astype(np.float64).copy()
+    N = T.shape[1] * T.shape[2] * T.shape[0]
+    losses, grads = [], []
+    for _ in range(iters):
+        S = oracle.surface_fwd(c, w.U, w.V, w.u, w.v, w.p, w.q)
+        d = S - T
+        losses.append(np.sum(d * d) / N)
+        g = oracle.surface_bwd(c, w.U, w.V, w.u, w.v, 2.0 * d / N, w.p, w.q)
+        grads.append(g)
+        c = c - lr * g
+    return np.array(losses), grads, c
+
+
+@pytest.mark.parametrize("n_s,iters", [(128, 60), (512, 25)])
+def test_fit_step_trajectory(n_s, iters):
+    truth, init = wl.config3_fit(n_s=n_s)
+    T64 = oracle.surface_fwd(truth.ctrl, truth.U, truth.V, truth.u, truth.v, 3, 3)
+    Tf = T64.astype(np.float32)
+    lr = 200.0
+    ref_loss, ref_grads, ref_ctrl = oracle_fit(init.ctrl, init, Tf.astype(np.float64), lr, iters)
+    ctrl = T(init.ctrl)
+    fitter = nb.SurfaceFitter(ctrl, T(init.U), T(init.V), T(init.u), T(init.v), T(Tf), 3, 3, lr)
+    # one un-graphed step first: loss, gradient and update at iteration 0
+    loss0 = torch.zeros(1, device=DEV)
+    fitter.step(loss0)
+    torch.cuda.synchronize()
+    assert abs(loss0.item() - ref_loss[0]) <= 1e-5 * ref_loss[0]
+    assert bwd_err(fitter.grad.cpu().numpy(), ref_grads[0], init.ctrl) <= BWD_TOL
+    # the remaining iterations in one CUDA graph
+    hist = fitter.run(iters - 1).cpu().numpy()
+    losses = np.concatenate([[loss0.item()], hist])
+    assert np.max(np.abs(losses - ref_loss)) / np.max(ref_loss) <= 1e-4
+    assert ref_loss[-1] < 0.5 * ref_loss[0]                   # it actually fits
+    got = ctrl.cpu().numpy()
+    assert np.max(np.abs(got - ref_ctrl)) / np.max(np.abs(ref_ctrl)) <= 1e-4
+
+
+def test_fit_step_batched_reduce_path_and_determinism():
+    """B > 1 with several tiles per surface (workspace reduce + SGD in the update kernel)."""
+    w = wl.surfaces("fitb", B=3, n=40, m=24, p=3, q=2, n_u=150, n_v=260, seed=31)
+    rng = np.random.default_rng(3)
+    Tf = (oracle.surface_fwd(w.ctrl, w.U, w.V, w.u, w.v, w.p, w.q)
+          + rng.normal(0, 0.01, (3, 150, 260, 3))).astype(np.float32)
+    lr = 50.0
+    ref_loss, ref_grads, ref_ctrl = oracle_fit(w.ctrl, w, Tf.astype(np.float64), lr, 3)
+    outs = []
+    for _ in range(2):
+        ctrl = T(w.ctrl)
+        fitter = nb.SurfaceFitter(ctrl, T(w.U), T(w.V), T(w.u), T(w.v), T(Tf), w.p, w.q, lr)
+        losses = fitter.run(3, graph=False).cpu().numpy()
+        outs.append((losses, ctrl.cpu().numpy(), fitter.grad.cpu().numpy()))
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])     # bitwise repeatable
+    assert np.max(np.abs(outs[0][0] - ref_loss)) / np.max(ref_loss) <= 1e-4
+    assert bwd_err(outs[0][2], ref_grads[-1], w.ctrl) <= BWD_TOL
+    assert np.max(np.abs(outs[0][1] - ref_ctrl)) / np.max(np.abs(ref_ctrl)) <= 1e-4

@@ -143,6 +143,19 @@ def config3(seed: int = 3) -> Surfaces:
     return surfaces("cfg3", 1, 32, 32, 3, 3, 512, 512, seed)
 
 
+def config3_fit(seed: int = 3, n: int = 32, n_s: int = 512):
+    """Config 3 (SGD surface fit, §4.2): a ground-truth NURBS (lattice + N(0,0.1),
+    w* ~ U(0.5,1.5)) whose surface is the target, and the initial guess P* + N(0, 0.05), w = 1
+    (SURVEY §8(d)). Returns (truth, init) Surfaces; the target points are computed by the caller."""
+    truth = surfaces("cfg3_truth", 1, n, n, 3, 3, n_s, n_s, seed)
+    rng = np.random.default_rng(seed + 100)
+    init_ctrl = truth.ctrl.copy()
+    init_ctrl[..., :3] += rng.normal(0.0, 0.05, size=init_ctrl[..., :3].shape).astype(f32)
+    init_ctrl[..., 3] = 1.0
+    init = Surfaces("cfg3_init", 3, 3, init_ctrl, truth.U, truth.V, truth.u, truth.v)
+    return truth, init
+
+
 def config4(seed: int = 4, B: int = 4096, knots_batched: bool = False) -> Surfaces:
     return surfaces("cfg4", B, 16, 16, 3, 3, 128, 128, seed, knots_batched)
 
