@@ -53,6 +53,9 @@ def lib():
         L.nurbs_ref_surface_bwd_eq89.argtypes = surf + [d, d]
         L.nurbs_ref_surface_bwd_selected.argtypes = surf + [d, c_int, i32, i32, i32, d]
         L.nurbs_ref_surface_dense.argtypes = [c_int] * 6 + [d, d, d, d, d, d, d]
+        L.nurbs_ref_basis_ders1.argtypes = [c_int, ctypes.c_double, c_int, d, d]
+        L.nurbs_ref_basis_ders1.restype = None
+        L.nurbs_ref_surface_derivs.argtypes = surf + [d, d, d]
         L.nurbs_ref_curve_fwd.argtypes = [c_int] * 5 + [d, d, d, d]
         L.nurbs_ref_curve_bwd.argtypes = [c_int] * 5 + [d, d, d, d, d]
         _lib = L
@@ -97,6 +100,24 @@ def basis_dense(n: int, p: int, U, u: float) -> np.ndarray:
     N = np.zeros(n)
     lib().nurbs_ref_basis_dense(n, p, _p(U), float(u), _p(N))
     return N
+
+
+def basis_ders1(s: int, u: float, p: int, U) -> np.ndarray:
+    """First derivatives of the p+1 non-zero basis functions at span s (NEXT-3)."""
+    U = _d(U)
+    dN = np.zeros(p + 1)
+    lib().nurbs_ref_basis_ders1(s, float(u), p, _p(U), _p(dN))
+    return dN
+
+
+def surface_derivs(ctrl, U, V, u, v, p: int, q: int, knots_batched: bool = False):
+    """(S, S_u, S_v) each [B][n_u][n_v][3] by Eq.7 and its v analogue."""
+    ctrl, U, V, u, v, dims = _surf_args(ctrl, U, V, u, v, p, q, knots_batched)
+    B, n_u, n_v = dims[0], dims[5], dims[6]
+    out, ou, ov = (np.zeros((B, n_u, n_v, 3)) for _ in range(3))
+    _chk(lib().nurbs_ref_surface_derivs(*dims, _p(ctrl), _p(U), _p(V), _p(u), _p(v), _p(out), _p(ou), _p(ov)),
+         "surface_derivs")
+    return out, ou, ov
 
 
 def spans(n: int, p: int, U, s) -> tuple[np.ndarray, np.ndarray]:

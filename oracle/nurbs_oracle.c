@@ -530,3 +530,79 @@ int nurbs_ref_curve_bwd(int B, int n, int p, int n_u, int knots_batched,
     }
     return REF_OK;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-3: first derivatives. Basis derivatives by differentiating Eq.4 once:             */
+/*   N'_{i,p}(u) = p N_{i,p-1}(u)/(U[i+p]-U[i]) - p N_{i+1,p-1}(u)/(U[i+p+1]-U[i+1])     */
+/* (0/0 := 0, R5), from the degree p-1 functions at the same span (Piegl–Tiller Eq.2.7).  */
+/* dN[r] = N'_{s-p+r,p}(u), r = 0..p.                                                    */
+/* ------------------------------------------------------------------------------------ */
+void nurbs_ref_basis_ders1(int s, double u, int p, const double* U, double* dN)
+{
+    if (p == 0) { dN[0] = 0.0; return; }
+    double Nm[REF_MAX_DEG + 1];
+    nurbs_ref_basis_funs(s, u, p - 1, U, Nm);  /* N_{s-p+1..s, p-1} */
+    for (int r = 0; r <= p; ++r) {
+        int i = s - p + r;
+        double a = 0.0, b = 0.0;
+        if (r >= 1) {
+            double d = U[i + p] - U[i];
+            a = (d != 0.0) ? Nm[r - 1] / d : 0.0;
+        }
+        if (r <= p - 1) {
+            double d = U[i + p + 1] - U[i + 1];
+            b = (d != 0.0) ? Nm[r] / d : 0.0;
+        }
+        dN[r] = p * (a - b);
+    }
+}
+
+/* Parametric derivatives, Eq.7 and its v analogue:                  */
+/*   S_,u = (NR_,u w - NR w_,u) / w^2,  NR_,u = sum N'_i N_j w P,  w_,u = sum N'_i N_j w   */
+/* out/out_u/out_v [B][n_u][n_v][3] (out nullable).                                      */
+int nurbs_ref_surface_derivs(int B, int n, int m, int p, int q, int n_u, int n_v, int knots_batched,
+                             const double* ctrl, const double* U, const double* V,
+                             const double* u, const double* v, double* out, double* out_u, double* out_v)
+{
+    if (p > REF_MAX_DEG || q > REF_MAX_DEG) return REF_E_ARG;
+    int st = check_common(B, n, m, p, q, n_u, n_v, knots_batched, ctrl, U, V, u, v);
+    if (st) return st;
+    double Nu[REF_MAX_DEG + 1], Nv[REF_MAX_DEG + 1], dNu[REF_MAX_DEG + 1], dNv[REF_MAX_DEG + 1];
+    for (int k = 0; k < B; ++k) {
+        const double* Uk = U + (knots_batched ? (size_t)k * (n + p + 1) : 0);
+        const double* Vk = V + (knots_batched ? (size_t)k * (m + q + 1) : 0);
+        const double* Pk = ctrl + (size_t)k * n * m * 4;
+        for (int a = 0; a < n_u; ++a) {
+            int su = nurbs_ref_find_span(n, p, Uk, u[a]);
+            nurbs_ref_basis_funs(su, u[a], p, Uk, Nu);
+            nurbs_ref_basis_ders1(su, u[a], p, Uk, dNu);
+            for (int b = 0; b < n_v; ++b) {
+                int sv = nurbs_ref_find_span(m, q, Vk, v[b]);
+                nurbs_ref_basis_funs(sv, v[b], q, Vk, Nv);
+                nurbs_ref_basis_ders1(sv, v[b], q, Vk, dNv);
+                double NR[3] = {0, 0, 0}, W = 0, NRu[3] = {0, 0, 0}, Wu = 0, NRv[3] = {0, 0, 0}, Wv = 0;
+                for (int r = 0; r <= p; ++r)
+                    for (int h = 0; h <= q; ++h) {
+                        const double* P = Pk + ((size_t)(su - p + r) * m + (sv - q + h)) * 4;
+                        double w = P[3];
+                        double c0 = Nu[r] * Nv[h], cu = dNu[r] * Nv[h], cv = Nu[r] * dNv[h];
+                        for (int c = 0; c < 3; ++c) {
+                            NR[c] += c0 * w * P[c];
+                            NRu[c] += cu * w * P[c];
+                            NRv[c] += cv * w * P[c];
+                        }
+                        W += c0 * w;
+                        Wu += cu * w;
+                        Wv += cv * w;
+                    }
+                size_t o = (((size_t)k * n_u + a) * n_v + b) * 3;
+                for (int c = 0; c < 3; ++c) {
+                    if (out) out[o + c] = NR[c] / W;
+                    out_u[o + c] = (NRu[c] * W - NR[c] * Wu) / (W * W);   /* Eq.7 */
+                    out_v[o + c] = (NRv[c] * W - NR[c] * Wv) / (W * W);
+                }
+            }
+        }
+    }
+    return REF_OK;
+}

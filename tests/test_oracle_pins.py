@@ -421,3 +421,79 @@ def test_error_paths():
     neg = ctrl.copy(); neg[0, 0, 0, 3] = 0.0
     with pytest.raises(oracle.OracleError):
         oracle.surface_fwd(neg, U, V, u, v, p, q)
+
+
+# ------------------------------------------------------------------------------ NEXT-3: derivatives
+def test_basis_ders_golden_and_sum_zero():
+    for c in load("basis_ders.json")["cases"]:
+        s = oracle.find_span(c["n"], c["p"], c["U"], c["u"])
+        assert s == c["span"]
+        np.testing.assert_allclose(oracle.basis_ders1(s, c["u"], c["p"], c["U"]), c["dN"], rtol=0, atol=1e-14)
+    rng = np.random.default_rng(40)
+    for _ in range(40):
+        p = int(rng.integers(1, 6))
+        n = int(rng.integers(p + 1, p + 10))
+        U = random_knots(rng, n, p)
+        for u in adversarial_params(U, rng, 10):
+            s = oracle.find_span(n, p, U, u)
+            assert abs(oracle.basis_ders1(s, u, p, U).sum()) <= 1e-10   # d/du (partition of unity)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5])
+def test_basis_ders_bernstein_and_fd(p):
+    U = [0.0] * (p + 1) + [1.0] * (p + 1)
+    for u in np.linspace(0.01, 0.99, 23):
+        d = oracle.basis_ders1(p, u, p, U)
+        ref = [math.comb(p, i) * ((i * u ** (i - 1) if i else 0.0) * (1 - u) ** (p - i)
+                                   - (u ** i) * ((p - i) * (1 - u) ** (p - i - 1) if p - i else 0.0))
+               for i in range(p + 1)]
+        np.testing.assert_allclose(d, ref, rtol=0, atol=1e-12)
+    rng = np.random.default_rng(41 + p)
+    n = p + 6
+    U = random_knots(rng, n, p, repeat=False)
+    h = 1e-7
+    for u in rng.uniform(0.06, 0.94, 30):
+        s = oracle.find_span(n, p, U, u)
+        if oracle.find_span(n, p, U, u - h) != s or oracle.find_span(n, p, U, u + h) != s:
+            continue
+        fd = (oracle.basis_funs(s, u + h, p, U) - oracle.basis_funs(s, u - h, p, U)) / (2 * h)
+        np.testing.assert_allclose(oracle.basis_ders1(s, u, p, U), fd, rtol=0, atol=1e-6)
+
+
+def test_surface_derivs_fd_and_value():
+    rng = np.random.default_rng(42)
+    for _ in range(6):
+        ctrl, U, V, u, v, p, q = random_surface(rng, B=2, batched=True)
+        # keep samples away from knots so the central differences stay in one span
+        u = np.array([x for x in np.linspace(0.03, 0.97, 9) if np.min(np.abs(U - x)) > 1e-4])
+        v = np.array([y for y in np.linspace(0.04, 0.96, 7) if np.min(np.abs(V - y)) > 1e-4])
+        S, Su, Sv = oracle.surface_derivs(ctrl, U, V, u, v, p, q, knots_batched=True)
+        np.testing.assert_allclose(S, oracle.surface_fwd(ctrl, U, V, u, v, p, q, True), rtol=0, atol=1e-15)
+        h = 1e-6
+        fu = (oracle.surface_fwd(ctrl, U, V, u + h, v, p, q, True) - oracle.surface_fwd(ctrl, U, V, u - h, v, p, q, True)) / (2 * h)
+        fv = (oracle.surface_fwd(ctrl, U, V, u, v + h, p, q, True) - oracle.surface_fwd(ctrl, U, V, u, v - h, p, q, True)) / (2 * h)
+        assert np.max(np.abs(Su - fu)) <= 1e-6 * max(1.0, np.max(np.abs(Su)))
+        assert np.max(np.abs(Sv - fv)) <= 1e-6 * max(1.0, np.max(np.abs(Sv)))
+
+
+def test_cylinder_normals_radial_and_plane_normal():
+    arc = [((1, 0), 1.0), ((1, 1), SQ2), ((0, 1), 1.0)]
+    ctrl = np.zeros((1, 3, 2, 4))
+    for i, ((x, y), w) in enumerate(arc):
+        for j, z in enumerate([0.0, 2.0]):
+            ctrl[0, i, j] = [x, y, z, w]
+    u = np.linspace(0, 1, 21)
+    v = np.linspace(0, 1, 5)
+    S, Su, Sv = oracle.surface_derivs(ctrl, [0, 0, 0, 1, 1, 1], [0, 0, 1, 1], u, v, 2, 1)
+    nrm = np.cross(Su, Sv)
+    nrm /= np.linalg.norm(nrm, axis=-1, keepdims=True)
+    radial = S.copy(); radial[..., 2] = 0
+    np.testing.assert_allclose(np.abs(np.sum(nrm * radial, axis=-1)), 1.0, atol=1e-12)
+    np.testing.assert_allclose(Sv[..., 2], 2.0, atol=1e-14)                             # z = 2v
+    # planar bilinear patch at z = 0: normal (0, 0, 1); reversed v order flips it
+    plane = np.zeros((1, 2, 2, 4)); plane[..., 3] = 1.0
+    plane[0, :, :, 0] = [[0, 0], [1, 1]]; plane[0, :, :, 1] = [[0, 1], [0, 1]]
+    _, pu, pv = oracle.surface_derivs(plane, [0, 0, 1, 1], [0, 0, 1, 1], [0.3], [0.6], 1, 1)
+    np.testing.assert_allclose(np.cross(pu, pv)[0, 0, 0], [0, 0, 1], atol=1e-15)
+    _, pu, pv = oracle.surface_derivs(plane[:, :, ::-1].copy(), [0, 0, 1, 1], [0, 0, 1, 1], [0.3], [0.6], 1, 1)
+    np.testing.assert_allclose(np.cross(pu, pv)[0, 0, 0], [0, 0, -1], atol=1e-15)
