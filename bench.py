@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--derivs", action="store_true", help="time the NEXT-3 derivative kernel instead")
     return ap.parse_args()
 
 
@@ -303,6 +304,50 @@ def run_fit(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- NEXT-3 derivatives
+def run_derivs(args, rank, world):
+    """NEXT-3: S, S_u, S_v and unit normals on config 4's workload (48 B/point written)."""
+    import numpy as np
+    import torch
+
+    import paper_2104_14547_b200 as nb
+    import workloads as wl
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = wl.config4() if args.config == 4 else wl.config5()
+    T_ = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctrl, U, V, u, v = T_(w.ctrl), T_(w.U), T_(w.V), T_(w.u), T_(w.v)
+    sh = nb.nurbs_shape(w.B, w.n, w.m, w.p, w.q, w.n_u, w.n_v, 0)
+    outs = [torch.empty((w.B, w.n_u, w.n_v, 3), dtype=torch.float32, device=dev) for _ in range(4)]
+    run = lambda: nb.nurbs_surface_derivs(sh, ctrl, U, V, u, v, outs[0], outs[1], outs[2], outs[3])
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        e0.record()
+        for _ in range(args.steps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    pts = w.points
+    byts = pts * 48 + w.ctrl.nbytes
+    peak, kind = load_peaks()
+    line = {"metric": "NURBS surface points/sec with parametric derivatives and normals (fp32, NEXT-3)",
+            "value": pts / (ms * 1e-3), "unit": "points/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": workload_name(args.config) + " -> S, S_u, S_v, normals"},
+            "roofline": {"bound": "hbm", "achieved": byts / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": byts / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": byts, "peak_kind": kind},
+            "gpu_launches": args.steps, "clocks": sampler.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -313,6 +358,8 @@ def main():
         return run_reference(args, rank, world)
     if args.config == 3:
         return run_fit(args, rank, world)
+    if args.derivs:
+        return run_derivs(args, rank, world)
 
     import torch
     import torch.distributed as dist

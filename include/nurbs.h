@@ -114,6 +114,17 @@ int    nurbs_surface_bwd(const nurbs_shape* shape, const float* ctrl,
 size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* shape);
 
 /* ---------------------------------------------------------------------------------------
+ * Parametric derivatives (Eq.7 P:196-209 and its v analogue) and unit normals
+ * (the offsetting input of §4.3) on the grid:
+ *     S_u = (NR_u w - NR w_u) / w^2,  S_v likewise,  n = S_u x S_v / |S_u x S_v|.
+ * out (nullable) receives S, out_u / out_v receive S_u / S_v, normals (nullable) receives n;
+ * all [B][n_u][n_v][3]. Spans and bases are computed in-kernel (no tables).
+ * --------------------------------------------------------------------------------------- */
+int    nurbs_surface_derivs(const nurbs_shape* shape, const float* ctrl,
+                            const float* U, const float* V, const float* u, const float* v,
+                            float* out, float* out_u, float* out_v, float* normals, void* stream);
+
+/* ---------------------------------------------------------------------------------------
  * Fused fitting step (the surface-fitting loop of §4.2, with Eq.14):
  * one SGD iteration of  L = mean over the n_u x n_v x B points of |S - T|^2  (R20) with
  * respect to the control points and weights, in place:

@@ -24,4 +24,6 @@ from .api import (  # noqa: F401
     fit_workspace_bytes,
     nurbs_surface_fit_step,
     SurfaceFitter,
+    nurbs_surface_derivs,
+    surface_derivs,
 )

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "NURBS_OK", 1: "NURBS_E_ARG", 2: "NURBS_E_UNSUPPORTED", 3: "N
 EXPORTS = ["nurbs_tables_bytes", "nurbs_tables", "nurbs_surface_fwd", "nurbs_surface_bwd",
            "nurbs_surface_bwd_workspace_bytes", "nurbs_curve_fwd", "nurbs_curve_bwd",
            "nurbs_curve_bwd_workspace_bytes", "nurbs_validate", "nurbs_strerror",
-           "nurbs_surface_fit_step", "nurbs_surface_fit_workspace_bytes",
+           "nurbs_surface_fit_step", "nurbs_surface_fit_workspace_bytes", "nurbs_surface_derivs",
            "nurbs_last_error_detail", "nurbs_abi_version"]
 
 
@@ -63,6 +63,7 @@ def load() -> ctypes.CDLL:
         "nurbs_validate": ([sh, P, P, P, P, P, P], I),
         "nurbs_surface_fit_step": ([sh, P, P, P, P, P, P, P, ctypes.c_float, P, P, P, S, P], I),
         "nurbs_surface_fit_workspace_bytes": ([sh], S),
+        "nurbs_surface_derivs": ([sh, P, P, P, P, P, P, P, P, P, P], I),
         "nurbs_strerror": ([I], ctypes.c_char_p),
         "nurbs_last_error_detail": ([], ctypes.c_char_p),
         "nurbs_abi_version": ([], I),

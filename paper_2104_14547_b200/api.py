@@ -104,6 +104,24 @@ def nurbs_surface_fit_step(sh, ctrl, U, V, u, v, tables, target, lr, grad_ctrl, 
           "nurbs_surface_fit_step")
 
 
+def nurbs_surface_derivs(sh, ctrl, U, V, u, v, out, out_u, out_v, normals, stream=None):
+    check(load().nurbs_surface_derivs(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v), _ptr(out),
+                                      _ptr(out_u), _ptr(out_v), _ptr(normals), _stream(stream)),
+          "nurbs_surface_derivs")
+
+
+def surface_derivs(ctrl, U, V, u, v, p: int, q: int, with_points: bool = True, with_normals: bool = True,
+                   stream=None):
+    """(S or None, S_u, S_v, normals or None), each [B][n_u][n_v][3] (NEXT-3, Eq.7)."""
+    sh = surface_shape(ctrl, U, u, v, p, q)
+    mk = lambda: torch.empty((sh.B, sh.n_u, sh.n_v, 3), dtype=_F32, device=ctrl.device)
+    out = mk() if with_points else None
+    ou, ov = mk(), mk()
+    nrm = mk() if with_normals else None
+    nurbs_surface_derivs(sh, ctrl, U, V, u, v, out, ou, ov, nrm, stream)
+    return out, ou, ov, nrm
+
+
 def fit_workspace_bytes(sh: nurbs_shape) -> int:
     return int(load().nurbs_surface_fit_workspace_bytes(ctypes.byref(sh)))
 

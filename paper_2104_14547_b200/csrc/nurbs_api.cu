@@ -335,6 +335,33 @@ int nurbs_surface_fit_step(const nurbs_shape* sh, float* ctrl, const float* U, c
   return launch_fit(g, ctrl, target, lr, grad_ctrl, loss, workspace, ws_bytes, s);
 }
 
+int nurbs_surface_derivs(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* u,
+                         const float* v, float* out, float* out_u, float* out_v, float* normals, void* stream) {
+  g_detail.clear();
+  int st = check_surface_shape(sh);
+  if (st) return st;
+  if (sh->B == 0 || sh->n_u == 0 || sh->n_v == 0) return NURBS_OK;
+  if (!ctrl || !U || !V || !u || !v || !out_u || !out_v) return fail(NURBS_E_ARG, "NULL pointer");
+  if (!aligned16(ctrl)) return fail(NURBS_E_ARG, "ctrl must be 16-byte aligned (float4 control points)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = surface_geo(sh, U, V, u, v);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns);
+  if (pl.grid > 0x7fffffffLL) return fail(NURBS_E_ARG, "grid of %lld CTAs too large", pl.grid);
+  Params prm{};
+  prm.B = g.B;
+  prm.r = g.r;
+  prm.c = g.c;
+  prm.ctrl = reinterpret_cast<const float4*>(ctrl);
+  prm.out = out;
+  prm.K = pl.K;
+  prm.NRB = pl.NRB;
+  prm.NCB = pl.NCB;
+  prm.T_rows = pl.T_rows;
+  cudaError_t e = nb::launch_derivs(prm, g.P, g.c.p, out_u, out_v, normals, s);
+  return e == cudaSuccess ? NURBS_OK : cuda_fail(e, "derivative kernel launch");
+}
+
 size_t nurbs_curve_bwd_workspace_bytes(const nurbs_shape* sh) {
   if (!sh || sh->B <= 0) return 0;
   return nb::make_plan(sh->B, 1, 0, 1, sh->n, sh->n_u).ws_bytes;

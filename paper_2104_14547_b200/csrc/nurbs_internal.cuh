@@ -162,6 +162,9 @@ cudaError_t launch_grid(const Params& prm, int mode, int P, int q, cudaStream_t 
 cudaError_t launch_reduce(const Params& prm, int P, cudaStream_t st);
 // fitting step: (reduce tile partials if needed) + SGD update of ctrl + loss = sum of the CTA partials
 cudaError_t launch_fit_update(const Params& prm, int P, cudaStream_t st);
+// NEXT-3 parametric derivatives (nurbs_derivs.cu): prm.out (nullable) receives S
+cudaError_t launch_derivs(const Params& prm, int P, int q, float* out_u, float* out_v, float* normals,
+                          cudaStream_t st);
 cudaError_t launch_tables(const Dir& r, const Dir& c, void* tables, const TabLayout& L,
                           cudaStream_t st);
 // status: device buffer of one unsigned long long, pre-set to ~0ull.

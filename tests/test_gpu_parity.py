@@ -412,3 +412,51 @@ def test_fit_step_batched_reduce_path_and_determinism():
     assert np.max(np.abs(outs[0][0] - ref_loss)) / np.max(ref_loss) <= 1e-4
     assert bwd_err(outs[0][2], ref_grads[-1], w.ctrl) <= BWD_TOL
     assert np.max(np.abs(outs[0][1] - ref_ctrl)) / np.max(np.abs(ref_ctrl)) <= 1e-4
+
+
+# --------------------------------------------------------------------------- parametric derivatives (NEXT-3)
+DER_TOL = 1e-4   # normwise: max|dS_gpu - dS_ref| / max|dS_ref| per surface (as R16 for gradients)
+
+
+def der_err(gpu, ref):
+    B = ref.shape[0]
+    e = np.abs(gpu.reshape(B, -1) - ref.reshape(B, -1)).max(axis=1)
+    return float(np.max(e / np.abs(ref.reshape(B, -1)).max(axis=1)))
+
+
+@pytest.mark.parametrize("case", ["cfg2", "cfg4", "batched", "deg15", "deg52", "ragged", "sparse", "cfg5net"])
+def test_surface_derivs_parity(case):
+    w = {"cfg2": lambda: wl.config2(),
+         "cfg4": lambda: wl.config4(B=6),
+         "batched": lambda: wl.config4(B=5, knots_batched=True),
+         "deg15": lambda: wl.surfaces("d15", B=2, n=9, m=11, p=1, q=5, n_u=40, n_v=70, seed=3),
+         "deg52": lambda: wl.surfaces("d52", B=2, n=11, m=7, p=5, q=2, n_u=33, n_v=130, seed=4),
+         "ragged": lambda: wl.surfaces("dr", B=2, n=10, m=9, p=3, q=3, n_u=45, n_v=301, seed=5),
+         "sparse": lambda: wl.surfaces("dsp", B=1, n=50, m=40, p=3, q=2, n_u=9, n_v=7, seed=6),
+         "cfg5net": lambda: wl.config5(n_u=700, n_v=600)}[case]()
+    S, Su, Sv, nrm = nb.surface_derivs(T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v), w.p, w.q)
+    torch.cuda.synchronize()
+    rS, rSu, rSv = oracle.surface_derivs(w.ctrl, w.U, w.V, w.u, w.v, w.p, w.q, w.knots_batched)
+    assert fwd_err(S.cpu().numpy(), rS, w.ctrl) <= FWD_TOL
+    assert der_err(Su.cpu().numpy(), rSu) <= DER_TOL
+    assert der_err(Sv.cpu().numpy(), rSv) <= DER_TOL
+    rn = np.cross(rSu, rSv)
+    rn /= np.linalg.norm(rn, axis=-1, keepdims=True)
+    cos = np.sum(nrm.cpu().numpy() * rn, axis=-1)
+    assert np.min(cos) >= 1 - 1e-4
+
+
+def test_cylinder_normals_on_gpu():
+    s2 = np.float32(np.sqrt(2.0) / 2.0)
+    arc = [((1, 0), 1.0), ((1, 1), s2), ((0, 1), 1.0)]
+    ctrl = np.zeros((1, 3, 2, 4), dtype=np.float32)
+    for i, ((x, y), wgt) in enumerate(arc):
+        for j, z in enumerate([0.0, 2.0]):
+            ctrl[0, i, j] = [x, y, z, wgt]
+    U = np.array([0, 0, 0, 1, 1, 1], np.float32)
+    V = np.array([0, 0, 1, 1], np.float32)
+    S, Su, Sv, nrm = nb.surface_derivs(T(ctrl), T(U), T(V), T(wl.uniform_grid(65)), T(wl.uniform_grid(9)), 2, 1)
+    S, nrm = S.cpu().numpy().astype(np.float64), nrm.cpu().numpy().astype(np.float64)
+    radial = S.copy(); radial[..., 2] = 0
+    radial /= np.linalg.norm(radial, axis=-1, keepdims=True)
+    assert np.max(np.abs(np.abs(np.sum(nrm * radial, axis=-1)) - 1.0)) <= 1e-5
