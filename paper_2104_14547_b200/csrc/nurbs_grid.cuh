@@ -87,8 +87,11 @@ struct B2Args {
   const float4* ctrl_s;   // this surface's control net
   float4* gctrl_s;        // this surface's gradient (direct mode)
   float4* slots;          // this tile's partial slot [T_rows][m] (reduce mode)
+  const float4* cband;    // the staged control band (rows from band_lo, columns from jlo)
   int m, cols, band_lo, sfirst, nspan;
-  bool fast, direct;
+  int cbw, jlo, ncol;     // band row stride, first column, columns staged
+  int lps;                // lanes per knot span in the fast path (power of 2, nspan*lps <= 32)
+  bool fast, direct, band_in_smem;
 };
 
 template <int Q>
@@ -98,24 +101,29 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
   const int t = threadIdx.x, m = a.m;
   auto store_dq = [&](int i, int j, float4 a4) {
     if (a.direct) {  // dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
-      const float4 c = __ldg(a.ctrl_s + (size_t)i * m + j);
+      const int jj = j - a.jlo;
+      float4 c;
+      if (a.band_in_smem && jj >= 0 && jj < a.ncol) c = a.cband[(size_t)(i - a.band_lo) * a.cbw + jj];
+      else c = __ldg(a.ctrl_s + (size_t)i * m + j);
       a.gctrl_s[(size_t)i * m + j] =
           make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
     } else {
       a.slots[(size_t)(i - a.band_lo) * m + j] = a4;
     }
   };
-  if (a.fast) {  // one warp per control row, one lane per knot span of the column block
+  if (a.fast) {  // one warp per control row; lps lanes per knot span of the column block
     const int lane = t & 31;
+    const int L = a.lps;
+    const int k = lane / L, sub = lane - k * L;
     for (int rr = (t >> 5); rr < nb; rr += kCompute / 32) {
       const int i = i0 + rr;
       const float4* Hr = a.Hring + ((i - a.band_lo) & (kHRing - 1)) * kCB;
       float4 c[Q + 1];
 #pragma unroll
       for (int h = 0; h <= Q; ++h) c[h] = f4(0.f);
-      if (lane < a.nspan) {  // lane k: span sfirst + k, columns [sst[k], sst[k+1])
-        const int e = a.sst[lane + 1];
-        for (int bb = a.sst[lane]; bb < e; ++bb) {
+      if (k < a.nspan) {  // span sfirst + k, columns [sst[k], sst[k+1]) strided over its lanes
+        const int e = a.sst[k + 1];
+        for (int bb = a.sst[k] + sub; bb < e; bb += L) {
           const float4 hv = Hr[bb];
           float nvv[NQ];
           const float4 q0 = *reinterpret_cast<const float4*>(a.Nv_s + bb * NQ);
@@ -128,15 +136,26 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
           for (int h = 0; h <= Q; ++h) c[h] = fma4v(nvv[h], hv, c[h]);
         }
       }
-      // lane L collects column j = sfirst - q + L: sum_h c[h] of lane L - h (span j + q - h)
+      for (int o = L >> 1; o > 0; o >>= 1) {  // sum the lanes of each span group (fixed order)
+#pragma unroll
+        for (int h = 0; h <= Q; ++h) {
+          c[h].x += __shfl_xor_sync(0xffffffffu, c[h].x, o);
+          c[h].y += __shfl_xor_sync(0xffffffffu, c[h].y, o);
+          c[h].z += __shfl_xor_sync(0xffffffffu, c[h].z, o);
+          c[h].w += __shfl_xor_sync(0xffffffffu, c[h].w, o);
+        }
+      }
+      // lane jj collects column j = sfirst - q + jj: sum_h c[h] of span jj - h (group (jj-h)*L)
       float4 d = f4(0.f);
 #pragma unroll
       for (int h = 0; h <= Q; ++h) {
-        const float vx = __shfl_up_sync(0xffffffffu, c[h].x, h);
-        const float vy = __shfl_up_sync(0xffffffffu, c[h].y, h);
-        const float vz = __shfl_up_sync(0xffffffffu, c[h].z, h);
-        const float vw = __shfl_up_sync(0xffffffffu, c[h].w, h);
-        if (lane >= h) d = make_float4(d.x + vx, d.y + vy, d.z + vz, d.w + vw);
+        const int ks = lane - h;
+        const int src = (ks >= 0 && ks < a.nspan) ? ks * L : 0;
+        const float vx = __shfl_sync(0xffffffffu, c[h].x, src);
+        const float vy = __shfl_sync(0xffffffffu, c[h].y, src);
+        const float vz = __shfl_sync(0xffffffffu, c[h].z, src);
+        const float vw = __shfl_sync(0xffffffffu, c[h].w, src);
+        if (ks >= 0 && ks < a.nspan) d = make_float4(d.x + vx, d.y + vy, d.z + vz, d.w + vw);
       }
       if (lane < a.nspan + Q) store_dq(i, a.sfirst - Q + lane, d);
       if (a.direct)  // columns this block does not touch
@@ -263,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     const int use_smem = ncol <= prm.CBW;
     misc[0] = jlo;
     misc[1] = use_smem;
+    misc[2] = ncol;
     if (use_smem) {
       const uint32_t rowb = (uint32_t)ncol * 16u;
       mbar_arrive_expect_tx(band_bar, rowb * band_rows);
@@ -365,8 +385,13 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     b2a.Hring = Hring; b2a.Nv_s = Nv_s; b2a.sv_s = sv_s; b2a.sst = sst;
     b2a.ctrl_s = ctrl_s; b2a.gctrl_s = prm.gctrl + (size_t)s * R.n * m;
     b2a.slots = prm.slots ? prm.slots + (((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows * m : nullptr;
+    b2a.cband = cband;
     b2a.m = m; b2a.cols = cols; b2a.band_lo = band_lo; b2a.sfirst = sfirst; b2a.nspan = nspan;
-    b2a.fast = b2fast; b2a.direct = prm.direct;
+    b2a.cbw = prm.CBW; b2a.jlo = jlo; b2a.ncol = misc[2];
+    int L = 32;
+    while (L > 1 && nspan * L > 32) L >>= 1;
+    b2a.lps = L;
+    b2a.fast = b2fast; b2a.direct = prm.direct; b2a.band_in_smem = band_in_smem;
   }
   auto Trow = [&](int i) -> float4 {
     float4 c[Q + 1];
@@ -386,7 +411,13 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   };
 
   // ---- B2 (backward): batches of completed rows in the H ring -> dQ (b2_batch_fn)
+#ifdef NB_EXP_NO_B2
+  auto b2_batch = [&](int i0, int nb) { (void)i0; (void)nb; };
+#elif defined(NB_EXP_B2_NOSYNC_WORK)
+  auto b2_batch = [&](int i0, int nb) { __syncthreads(); __syncthreads(); (void)i0; (void)nb; };
+#else
   auto b2_batch = [&](int i0, int nb) { b2_batch_fn<Q>(b2a, i0, nb); };
+#endif
   int b2_next = band_lo;  // first completed control row not yet reduced by B2
   // row i complete (uniform across the CTA): H(i) -> ring. The fast variant never reduces
   // (the stage loop guarantees ring capacity); the checked one reduces a full ring.
