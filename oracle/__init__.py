@@ -56,6 +56,9 @@ def lib():
         L.nurbs_ref_basis_ders1.argtypes = [c_int, ctypes.c_double, c_int, d, d]
         L.nurbs_ref_basis_ders1.restype = None
         L.nurbs_ref_surface_derivs.argtypes = surf + [d, d, d]
+        pts = [c_int] * 7 + [d, d, d, d]
+        L.nurbs_ref_surface_fwd_points.argtypes = pts + [d]
+        L.nurbs_ref_surface_bwd_points.argtypes = pts + [d, d]
         L.nurbs_ref_curve_fwd.argtypes = [c_int] * 5 + [d, d, d, d]
         L.nurbs_ref_curve_bwd.argtypes = [c_int] * 5 + [d, d, d, d, d]
         _lib = L
@@ -183,6 +186,32 @@ def surface_dense(ctrl2d, U, V, u, v, p, q, jacobian: bool = False):
     _chk(lib().nurbs_ref_surface_dense(n, m, p, q, len(u), len(v), _p(ctrl), _p(U), _p(V), _p(u), _p(v),
                                        _p(out), _p(J) if jacobian else None), "surface_dense")
     return out, J
+
+
+def _pts_args(ctrl, U, V, uv, p, q, knots_batched):
+    ctrl, U, V, uv = _d(ctrl), _d(U), _d(V), _d(uv)
+    B, n, m, four = ctrl.shape
+    assert four == 4 and uv.shape[0] == B and uv.shape[2] == 2
+    return ctrl, U, V, uv, (B, n, m, p, q, uv.shape[1], int(knots_batched))
+
+
+def surface_fwd_points(ctrl, U, V, uv, p: int, q: int, knots_batched: bool = False) -> np.ndarray:
+    """Paired points (NEXT-1): out [B][N][3] at uv [B][N][2] (Eq.3 per point)."""
+    ctrl, U, V, uv, dims = _pts_args(ctrl, U, V, uv, p, q, knots_batched)
+    out = np.zeros((dims[0], dims[5], 3))
+    _chk(lib().nurbs_ref_surface_fwd_points(*dims, _p(ctrl), _p(U), _p(V), _p(uv), _p(out)), "fwd_points")
+    return out
+
+
+def surface_bwd_points(ctrl, U, V, uv, gout, p: int, q: int, knots_batched: bool = False) -> np.ndarray:
+    """Paired points (NEXT-1): grad [B][n][m][4] by the literal Eq.8/9 (Form E)."""
+    ctrl, U, V, uv, dims = _pts_args(ctrl, U, V, uv, p, q, knots_batched)
+    g = _d(gout)
+    assert g.shape == (dims[0], dims[5], 3)
+    grad = np.zeros((dims[0], dims[1], dims[2], 4))
+    _chk(lib().nurbs_ref_surface_bwd_points(*dims, _p(ctrl), _p(U), _p(V), _p(uv), _p(g), _p(grad)),
+         "bwd_points")
+    return grad
 
 
 def curve_fwd(ctrl, U, u, p: int, knots_batched: bool = False) -> np.ndarray:

@@ -606,3 +606,124 @@ int nurbs_ref_surface_derivs(int B, int n, int m, int p, int q, int n_u, int n_v
     }
     return REF_OK;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-1: paired (scattered) parameter points. Every point k of surface b carries its   */
+/* own (u, v) = uv[b][k] (§3.1: S(u,v) for any (u,v) in the domain; Alg.1's    */
+/* per-point span and basis). Same steps as the grid functions above: FindSpan */
+/* (A2.1), BasisFuns (A2.2), the rational sum of Eq.3 (R1).         */
+/* uv [B][N][2]; out / gout [B][N][3]; grad [B][n][m][4].                               */
+/* ------------------------------------------------------------------------------------ */
+static int check_points(int B, int n, int m, int p, int q, int N, int kb, const double* ctrl,
+                        const double* U, const double* V, const double* uv)
+{
+    if (B < 0 || N < 0 || p > REF_MAX_DEG || q > REF_MAX_DEG) return REF_E_ARG;
+    int nU = n + p + 1, nV = m + q + 1;
+    for (int k = 0; k < (kb ? B : (B > 0 ? 1 : 0)); ++k) {
+        int st = nurbs_ref_check_knots(n, p, U + (size_t)k * nU);
+        if (st) return st;
+        st = nurbs_ref_check_knots(m, q, V + (size_t)k * nV);
+        if (st) return st;
+    }
+    for (int k = 0; k < B; ++k) {
+        const double* Uk = U + (kb ? (size_t)k * nU : 0);
+        const double* Vk = V + (kb ? (size_t)k * nV : 0);
+        for (int t = 0; t < N; ++t) {
+            const double* x = uv + ((size_t)k * N + t) * 2;
+            if (nurbs_ref_find_span(n, p, Uk, x[0]) < 0) return REF_E_DOMAIN;
+            if (nurbs_ref_find_span(m, q, Vk, x[1]) < 0) return REF_E_DOMAIN;
+        }
+    }
+    for (size_t t = 0; t < (size_t)B * n * m; ++t)
+        if (!(ctrl[4 * t + 3] > 0.0)) return REF_E_WEIGHT;   /* R15 */
+    return REF_OK;
+}
+
+/* Forward at paired points: Eq.3 via P:138-140, point by point (Alg.1). */
+int nurbs_ref_surface_fwd_points(int B, int n, int m, int p, int q, int N, int knots_batched,
+                                 const double* ctrl, const double* U, const double* V,
+                                 const double* uv, double* out)
+{
+    int st = check_points(B, n, m, p, q, N, knots_batched, ctrl, U, V, uv);
+    if (st) return st;
+    double Nu[REF_MAX_DEG + 1], Nv[REF_MAX_DEG + 1];
+    for (int k = 0; k < B; ++k) {
+        const double* Uk = U + (knots_batched ? (size_t)k * (n + p + 1) : 0);
+        const double* Vk = V + (knots_batched ? (size_t)k * (m + q + 1) : 0);
+        const double* Pk = ctrl + (size_t)k * n * m * 4;
+        for (int t = 0; t < N; ++t) {
+            const double u = uv[((size_t)k * N + t) * 2], v = uv[((size_t)k * N + t) * 2 + 1];
+            int su = nurbs_ref_find_span(n, p, Uk, u);
+            int sv = nurbs_ref_find_span(m, q, Vk, v);
+            nurbs_ref_basis_funs(su, u, p, Uk, Nu);
+            nurbs_ref_basis_funs(sv, v, q, Vk, Nv);
+            double Sw[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int r = 0; r <= p; ++r)
+                for (int h = 0; h <= q; ++h) {
+                    const double* P = Pk + ((size_t)(su - p + r) * m + (sv - q + h)) * 4;
+                    double Nrh = Nu[r] * Nv[h];
+                    Sw[0] += Nrh * (P[3] * P[0]);
+                    Sw[1] += Nrh * (P[3] * P[1]);
+                    Sw[2] += Nrh * (P[3] * P[2]);
+                    Sw[3] += Nrh * P[3];
+                }
+            double* o = out + ((size_t)k * N + t) * 3;
+            o[0] = Sw[0] / Sw[3];
+            o[1] = Sw[1] / Sw[3];
+            o[2] = Sw[2] / Sw[3];
+        }
+    }
+    return REF_OK;
+}
+
+/* Backward at paired points: the literal Eq.8 / Eq.9 (Form E) with the */
+/* upstream factor (R11), accumulated over the points in index order t = 0..N-1.       */
+int nurbs_ref_surface_bwd_points(int B, int n, int m, int p, int q, int N, int knots_batched,
+                                 const double* ctrl, const double* U, const double* V,
+                                 const double* uv, const double* gout, double* grad)
+{
+    int st = check_points(B, n, m, p, q, N, knots_batched, ctrl, U, V, uv);
+    if (st) return st;
+    memset(grad, 0, sizeof(double) * (size_t)B * n * m * 4);
+    double Nu[REF_MAX_DEG + 1], Nv[REF_MAX_DEG + 1];
+    for (int k = 0; k < B; ++k) {
+        const double* Uk = U + (knots_batched ? (size_t)k * (n + p + 1) : 0);
+        const double* Vk = V + (knots_batched ? (size_t)k * (m + q + 1) : 0);
+        const double* Pk = ctrl + (size_t)k * n * m * 4;
+        double* Gk = grad + (size_t)k * n * m * 4;
+        for (int t = 0; t < N; ++t) {
+            const double u = uv[((size_t)k * N + t) * 2], v = uv[((size_t)k * N + t) * 2 + 1];
+            int su = nurbs_ref_find_span(n, p, Uk, u);
+            int sv = nurbs_ref_find_span(m, q, Vk, v);
+            nurbs_ref_basis_funs(su, u, p, Uk, Nu);
+            nurbs_ref_basis_funs(sv, v, q, Vk, Nv);
+            double NR[3] = {0.0, 0.0, 0.0}, W = 0.0;   /* Eq.6 */
+            for (int r = 0; r <= p; ++r)
+                for (int h = 0; h <= q; ++h) {
+                    const double* P = Pk + ((size_t)(su - p + r) * m + (sv - q + h)) * 4;
+                    double Nrh = Nu[r] * Nv[h];
+                    NR[0] += Nrh * P[3] * P[0];
+                    NR[1] += Nrh * P[3] * P[1];
+                    NR[2] += Nrh * P[3] * P[2];
+                    W += Nrh * P[3];
+                }
+            const double* g = gout + ((size_t)k * N + t) * 3;
+            for (int r = 0; r <= p; ++r)
+                for (int h = 0; h <= q; ++h) {
+                    size_t idx = (size_t)(su - p + r) * m + (sv - q + h);
+                    const double* P = Pk + idx * 4;
+                    double Nrh = Nu[r] * Nv[h];
+                    double R = Nrh * P[3] / W;                                   /* Eq.8 */
+                    double* d = Gk + idx * 4;
+                    d[0] += R * g[0];
+                    d[1] += R * g[1];
+                    d[2] += R * g[2];
+                    double dw = 0.0;
+                    for (int c = 0; c < 3; ++c)
+                        dw += g[c] * (Nrh * P[c] * W - NR[c] * Nrh) / (W * W);    /* Eq.9 */
+                    d[3] += dw;
+                }
+        }
+    }
+    return REF_OK;
+}

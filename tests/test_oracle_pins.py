@@ -497,3 +497,99 @@ def test_cylinder_normals_radial_and_plane_normal():
     np.testing.assert_allclose(np.cross(pu, pv)[0, 0, 0], [0, 0, 1], atol=1e-15)
     _, pu, pv = oracle.surface_derivs(plane[:, :, ::-1].copy(), [0, 0, 1, 1], [0, 0, 1, 1], [0.3], [0.6], 1, 1)
     np.testing.assert_allclose(np.cross(pu, pv)[0, 0, 0], [0, 0, -1], atol=1e-15)
+
+
+# ---------------------------------------------------------------- NEXT-1: paired points
+def random_uv(rng, U, V, p, q, B, N):
+    """Scattered (u, v) in the domain, with knot hits and both ends mixed in."""
+    uv = rng.uniform(0, 1, size=(B, N, 2))
+    Ub = np.asarray(U).reshape(-1, np.shape(U)[-1])
+    Vb = np.asarray(V).reshape(-1, np.shape(V)[-1])
+    for k in range(B):
+        Uk, Vk = Ub[k % len(Ub)], Vb[k % len(Vb)]
+        hits = [(Uk[rng.integers(p, len(Uk) - p)], Vk[rng.integers(q, len(Vk) - q)]) for _ in range(N // 4)]
+        for t, (a, b) in enumerate(hits):
+            uv[k, 4 * t] = (a, b)
+        if N >= 3:
+            uv[k, 1] = (0.0, 1.0)
+            uv[k, 2] = (1.0, 0.0)
+    return uv
+
+
+def test_points_at_grid_coordinates_equal_grid_oracle():
+    """The grid is the special case uv[k][a*n_v+b] = (u_a, v_b): identical forward, and the
+    same gradient (P:154-163 per point; the grid functions are pinned above)."""
+    rng = np.random.default_rng(21)
+    for trial in range(6):
+        ctrl, U, V, u, v, p, q = random_surface(rng, B=2, batched=bool(trial % 2))
+        uu, vv = np.meshgrid(u, v, indexing="ij")
+        uv = np.broadcast_to(np.stack([uu.ravel(), vv.ravel()], -1), (2, uu.size, 2)).copy()
+        out = oracle.surface_fwd_points(ctrl, U, V, uv, p, q, bool(trial % 2))
+        ref = oracle.surface_fwd(ctrl, U, V, u, v, p, q, bool(trial % 2))
+        assert np.array_equal(out, ref.reshape(2, -1, 3))
+        g = rng.normal(size=(2, len(u), len(v), 3))
+        G = oracle.surface_bwd_points(ctrl, U, V, uv, g.reshape(2, -1, 3), p, q, bool(trial % 2))
+        E = oracle.surface_bwd(ctrl, U, V, u, v, g, p, q, bool(trial % 2), form="E")
+        np.testing.assert_allclose(G, E, rtol=0, atol=1e-14 * np.max(np.abs(E)))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_points_backward_finite_differences(seed):
+    rng = np.random.default_rng(200 + seed)
+    ctrl, U, V, _, _, p, q = random_surface(rng, B=2, batched=bool(seed % 2))
+    uv = random_uv(rng, U, V, p, q, 2, 23)
+    g = rng.normal(size=(2, 23, 3))
+    an = oracle.surface_bwd_points(ctrl, U, V, uv, g, p, q, bool(seed % 2))
+    fd = np.zeros_like(ctrl)
+    h = 1e-6
+    for idx in np.ndindex(ctrl.shape):
+        cp, cm = ctrl.copy(), ctrl.copy()
+        cp[idx] += h
+        cm[idx] -= h
+        fd[idx] = (np.sum(oracle.surface_fwd_points(cp, U, V, uv, p, q, bool(seed % 2)) * g)
+                   - np.sum(oracle.surface_fwd_points(cm, U, V, uv, p, q, bool(seed % 2)) * g)) / (2 * h)
+    assert np.max(np.abs(an - fd)) / np.max(np.abs(fd)) <= 1e-7
+
+
+def test_points_dense_brute_force_and_cylinder():
+    """Each paired point against the literal Eq.4/5 dense evaluation and its Jacobian J^T g
+    (P:238), and the exact cylinder x^2 + y^2 = 1, z = 2v at scattered points."""
+    rng = np.random.default_rng(22)
+    for _ in range(4):
+        ctrl, U, V, _, _, p, q = random_surface(rng, B=1)
+        uv = random_uv(rng, U, V, p, q, 1, 9)
+        g = rng.normal(size=(1, 9, 3))
+        out = oracle.surface_fwd_points(ctrl, U, V, uv, p, q)
+        G = oracle.surface_bwd_points(ctrl, U, V, uv, g, p, q)
+        acc = np.zeros_like(G[0])
+        for t in range(9):
+            o, J = oracle.surface_dense(ctrl[0], U, V, uv[0, t, :1], uv[0, t, 1:], p, q, jacobian=True)
+            np.testing.assert_allclose(out[0, t], o[0, 0], rtol=0, atol=1e-14)
+            acc += (J.T @ g[0, t]).reshape(acc.shape)
+        np.testing.assert_allclose(G[0], acc, rtol=0, atol=1e-13 * np.max(np.abs(acc)))
+    arc = [((1, 0), 1.0), ((1, 1), SQ2), ((0, 1), 1.0)]
+    cyl = np.zeros((1, 3, 2, 4))
+    for i, ((x, y), w) in enumerate(arc):
+        for j, z in enumerate([0.0, 2.0]):
+            cyl[0, i, j] = [x, y, z, w]
+    uv = rng.uniform(0, 1, size=(1, 200, 2))
+    out = oracle.surface_fwd_points(cyl, [0, 0, 0, 1, 1, 1], [0, 0, 1, 1], uv, 2, 1)
+    assert np.max(np.abs(np.hypot(out[0, :, 0], out[0, :, 1]) - 1.0)) <= 1e-12
+    np.testing.assert_allclose(out[0, :, 2], 2 * uv[0, :, 1], atol=1e-14)
+
+
+def test_points_backward_invariants_and_errors():
+    rng = np.random.default_rng(23)
+    ctrl, U, V, _, _, p, q = random_surface(rng, B=1)
+    uv = random_uv(rng, U, V, p, q, 1, 40)
+    g = rng.normal(size=(1, 40, 3))
+    G = oracle.surface_bwd_points(ctrl, U, V, uv, g, p, q)[0]
+    S = oracle.surface_fwd_points(ctrl, U, V, uv, p, q)
+    sc = np.sum(np.abs(g))
+    np.testing.assert_allclose(G[..., :3].sum(axis=(0, 1)), g[0].sum(axis=0), atol=1e-13 * sc)
+    assert abs(np.sum(ctrl[0, ..., 3] * G[..., 3])) <= 1e-13 * sc
+    assert abs(np.sum(ctrl[0, ..., :3] * G[..., :3]) - np.sum(g * S)) <= 1e-13 * sc
+    bad = uv.copy(); bad[0, 5, 1] = 1.5
+    with pytest.raises(oracle.OracleError):
+        oracle.surface_fwd_points(ctrl, U, V, bad, p, q)
+    assert oracle.surface_fwd_points(ctrl, U, V, uv[:, :0], p, q).shape == (1, 0, 3)

@@ -165,3 +165,59 @@ def config5(seed: int = 5, n_u: int = 8192, n_v: int = 8192) -> Surfaces:
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+
+
+@dataclass
+class PairedSurfaces:
+    """Paired (scattered) parameter points (NEXT-1): point t of surface k sits at uv[k][t]."""
+    name: str
+    p: int
+    q: int
+    ctrl: np.ndarray          # [B][n][m][4]
+    U: np.ndarray             # [n+p+1] or [B][n+p+1]
+    V: np.ndarray
+    uv: np.ndarray            # [B][N][2]
+    knots_batched: bool = False
+
+    @property
+    def B(self): return self.ctrl.shape[0]
+    @property
+    def n(self): return self.ctrl.shape[1]
+    @property
+    def m(self): return self.ctrl.shape[2]
+    @property
+    def N(self): return self.uv.shape[1]
+    @property
+    def points(self): return self.B * self.N
+
+    def grad_out(self, seed: int | None = None) -> np.ndarray:
+        rng = np.random.default_rng(seed if seed is not None else 2000 + sum(self.name.encode()))
+        return normal(rng, (self.B, self.N, 3))
+
+
+def paired(name: str, B: int, n: int, m: int, p: int, q: int, N: int, seed: int,
+           knots_batched: bool = False, knot_hits: bool = True) -> PairedSurfaces:
+    """Lattice nets (as `surfaces`) with N scattered points per surface, uv ~ U(0,1)^2 in fp32
+    (point-cloud parameters, SplineNet/ParSeNet style). With `knot_hits`, every 16th
+    point is moved onto a knot pair and points 1, 2 onto the corners (0,1), (1,0)."""
+    base = surfaces(name, B, n, m, p, q, 1, 1, seed, knots_batched)
+    rng = np.random.default_rng(seed + 7)
+    uv = rng.uniform(0.0, 1.0, size=(B, N, 2)).astype(f32)
+    if knot_hits and N > 0:
+        Ub = base.U.reshape(-1, base.U.shape[-1])
+        Vb = base.V.reshape(-1, base.V.shape[-1])
+        t = np.arange(0, N, 16)
+        for k in range(B):
+            Uk, Vk = Ub[k % len(Ub)], Vb[k % len(Vb)]
+            uv[k, t, 0] = Uk[rng.integers(p, len(Uk) - p, size=len(t))]
+            uv[k, t, 1] = Vk[rng.integers(q, len(Vk) - q, size=len(t))]
+        if N >= 3:
+            uv[:, 1] = (0.0, 1.0)
+            uv[:, 2] = (1.0, 0.0)
+    return PairedSurfaces(name, p, q, base.ctrl, base.U, base.V, uv, knots_batched)
+
+
+def config4_paired(seed: int = 41, B: int = 4096, N: int = 16384, knots_batched: bool = False):
+    """The paired-points throughput workload: cfg4's nets (4096 bicubic 16x16,
+    13 spans) with 16384 scattered points each = 67,108,864 points, the same count as cfg4."""
+    return paired("cfg4p", B, 16, 16, 3, 3, N, seed, knots_batched)
