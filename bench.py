@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--derivs", action="store_true", help="time the NEXT-3 derivative kernel instead")
+    ap.add_argument("--paired", action="store_true",
+                    help="time the NEXT-1 paired-points path on cfg4p (cfg4's nets, 16384 scattered points each)")
     return ap.parse_args()
 
 
@@ -348,6 +350,123 @@ def run_derivs(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- NEXT-1 paired points
+FP32_FMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: FFMA2 fma-pipe peak at clocks.max.sm
+
+
+def paired_flops_per_point(p, q, bwd):
+    """Algorithmic flops of one paired point: A2.2 basis per direction
+    sum_j (2 + 4j), the separable homogeneous sum 8((p+1)(q+1) + (p+1)), divide 4; the
+    backward adds G (10) and the (p+1)(q+1) float4 accumulations 8(p+1)(q+1) + 4(p+1)."""
+    basis = sum(2 + 4 * j for j in range(1, p + 1)) + sum(2 + 4 * j for j in range(1, q + 1))
+    fwd = basis + 8 * ((p + 1) * (q + 1) + (p + 1)) + 4
+    return fwd + (10 + 8 * (p + 1) * (q + 1) + 4 * (p + 1) if bwd else 0)
+
+
+def run_paired(args, rank, world):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_14547_b200 as nb
+    import workloads as wl
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = wl.config4_paired(seed=41 + 1000 * rank)
+    T_ = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctrl, U, V, uv = T_(w.ctrl), T_(w.U), T_(w.V), T_(w.uv)
+    gout = T_(w.grad_out())
+    sh = nb.nurbs_shape(w.B, w.n, w.m, w.p, w.q, w.N, 1, 0)
+    out = torch.empty((w.B, w.N, 3), dtype=torch.float32, device=dev)
+    grad = torch.empty_like(ctrl)
+    gU, gV = torch.empty_like(U), torch.empty_like(V)
+    ws_bytes = nb.points_workspace_bytes(sh)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    fwd = lambda: nb.nurbs_surface_points_fwd(sh, ctrl, U, V, uv, out, stream)
+    bwd = lambda: nb.nurbs_surface_points_bwd(sh, ctrl, U, V, uv, gout, grad, gU, gV, ws, ws_bytes, stream)
+    for _ in range(args.warmup):
+        fwd(); bwd()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    K = args.steps
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K + 1)]
+    sampler = ClockSampler(local)
+    with sampler:
+        ev[0].record(stream)
+        for k in range(K):
+            fwd()
+            ev[2 * k + 1].record(stream)
+            bwd()
+            ev[2 * k + 2].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([ev[0].elapsed_time(ev[2 * K]),
+                      sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(K)) / K,
+                      sum(ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(K)) / K],
+                     dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, fwd_ms, bwd_ms = t.tolist()
+    ms = total_ms / K
+    pts = w.points
+    hbm_peak, peak_kind = load_peaks()
+    ctrl_b = w.ctrl.nbytes
+    fwd_bytes = pts * 20 + ctrl_b                          # uv 8 + out 12 per point
+    bwd_bytes = pts * 20 + 2 * ctrl_b + ws_bytes * 2       # uv 8 + dL/dS 12; ctrl in, grad out
+    fl_f, fl_b = paired_flops_per_point(w.p, w.q, False), paired_flops_per_point(w.p, w.q, True)
+    def legs(ms_, byts, fl):
+        gbs = byts / (ms_ * 1e-3) / 1e9
+        tf = pts * fl / (ms_ * 1e-3) / 1e12
+        return {"ms": ms_, "bytes": byts, "gbs": gbs, "hbm_frac": gbs / hbm_peak, "flops_per_point": fl,
+                "tflops": tf, "alu_frac": tf / FP32_FMA_TFLOPS}
+    lf, lb = legs(fwd_ms, fwd_bytes, fl_f), legs(bwd_ms, bwd_bytes, fl_b)
+    dom, dname = (lb, "nurbs_points_bwd_kernel<3,3>") if bwd_ms >= fwd_ms else (lf, "nurbs_points_fwd_kernel<3,3>")
+    if dom["alu_frac"] >= dom["hbm_frac"]:
+        roof = {"bound": "alu", "achieved": dom["tflops"], "peak": FP32_FMA_TFLOPS, "unit": "TFLOP/s",
+                "frac": dom["alu_frac"], "peak_kind": "fp32 FFMA2 fma-pipe: 148 SMs x 128 lanes x 2 x 1.965 GHz"}
+    else:
+        roof = {"bound": "hbm", "achieved": dom["gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": dom["hbm_frac"],
+                "peak_kind": f"{peak_kind} copy bandwidth"}
+    roof.update({"kernel": dname, "traffic": None, "fwd": lf, "bwd": lb})
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        done, used = 0, 0.0
+        while used < args.cpu_seconds and done < 64:
+            sub = slice(done, done + 4)
+            t0 = time.perf_counter()
+            oracle.surface_fwd_points(w.ctrl[sub], w.U, w.V, w.uv[sub], w.p, w.q)
+            oracle.surface_bwd_points(w.ctrl[sub], w.U, w.V, w.uv[sub], w.grad_out()[sub], w.p, w.q)
+            used += time.perf_counter() - t0
+            done += 4
+        cpu = {"value": done * w.N / used, "unit": "points/s", "cores": 1, "kind": "oracle",
+               "sample": f"cfg4p fwd+bwd on {done} of 4096 surfaces ({done * w.N} points), fp64, 1 thread",
+               "seconds": used}
+    if rank == 0:
+        line = {"metric": "NURBS surface points/sec fwd+bwd at paired (scattered) parameter points (fp32, NEXT-1)",
+                "value": pts * world / (ms * 1e-3), "unit": "points/s", "n_gpus": world, "steps": K,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (cfg4 lattice nets, uv ~ U(0,1)^2 with knot hits, N(0,1) dL/dS)",
+                "config": {"workload": "cfg4p: 4096 bicubic 16x16 NURBS surfaces x 16384 scattered (u,v) points, fwd+bwd",
+                           "points_per_step": pts * world, "parallelism": f"batch-sharded x{world}, no collective",
+                           "l2": "inputs larger than L2 (uv 537 MB, out and dL/dS 805 MB each), no flush"},
+                "fwd_points_per_s": pts * world / (fwd_ms * 1e-3), "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": None,
+                "gpu_launches": K * (2 + (1 if ws_bytes > 0 else 0)), "clocks": sampler.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # --------------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -360,6 +479,8 @@ def main():
         return run_fit(args, rank, world)
     if args.derivs:
         return run_derivs(args, rank, world)
+    if args.paired:
+        return run_paired(args, rank, world)
 
     import torch
     import torch.distributed as dist

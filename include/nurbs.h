@@ -143,6 +143,33 @@ int    nurbs_surface_fit_step(const nurbs_shape* shape, float* ctrl,
 size_t nurbs_surface_fit_workspace_bytes(const nurbs_shape* shape);
 
 /* ---------------------------------------------------------------------------------------
+ * Paired (scattered) parameter points (NEXT-1): point t of surface k is evaluated at its own
+ * (u, v) = uv[k][t] — S(u, v) anywhere in the domain with the per-point span and
+ * basis of Alg.1, the same Eq.3 sum and Eq.8/9 gradient as the grid calls.
+ *   shape.n_u = N (points per surface), shape.n_v must be 1; tables are not used.
+ *   uv        [B][N][2]  (u, v) pairs in any order, each inside the domain (no sorting needed).
+ *   out       [B][N][3];  grad_out [B][N][3];  grad_ctrl [B][n][m][4] OVERWRITTEN;
+ *   grad_U / grad_V nullable, zero-filled.
+ * The backward sorts each CTA's points by knot cell in shared memory and reduces in a fixed
+ * order: deterministic, no atomics. It needs (n-p)(m-q) <= 65535 knot cells and a control
+ * net small enough for its shared-memory reduction (about n*m <= 1400 for p = q = 3),
+ * otherwise it returns NURBS_E_UNSUPPORTED. Workspace: nurbs_surface_points_bwd_workspace_bytes.
+ * nurbs_validate_points is the checked mode (knots, every (u, v) in the domain, weights);
+ * it SYNCHRONIZES. NURBS_CHECK=1 runs it inside fwd/bwd.
+ * --------------------------------------------------------------------------------------- */
+int    nurbs_surface_points_fwd(const nurbs_shape* shape, const float* ctrl,
+                                const float* U, const float* V, const float* uv,
+                                float* out, void* stream);
+int    nurbs_surface_points_bwd(const nurbs_shape* shape, const float* ctrl,
+                                const float* U, const float* V, const float* uv,
+                                const float* grad_out, float* grad_ctrl,
+                                float* grad_U, float* grad_V,
+                                void* workspace, size_t ws_bytes, void* stream);
+size_t nurbs_surface_points_bwd_workspace_bytes(const nurbs_shape* shape);
+int    nurbs_validate_points(const nurbs_shape* shape, const float* ctrl, const float* U,
+                             const float* V, const float* uv, void* stream);
+
+/* ---------------------------------------------------------------------------------------
  * Curves: shape.m = 1, shape.q = 0. Same semantics as the surface calls.
  * --------------------------------------------------------------------------------------- */
 int    nurbs_curve_fwd(const nurbs_shape* shape, const float* ctrl, const float* U,

@@ -26,4 +26,11 @@ from .api import (  # noqa: F401
     SurfaceFitter,
     nurbs_surface_derivs,
     surface_derivs,
+    points_shape,
+    points_workspace_bytes,
+    nurbs_surface_points_fwd,
+    nurbs_surface_points_bwd,
+    nurbs_validate_points,
+    surface_points_fwd,
+    surface_points_bwd,
 )

@@ -23,7 +23,8 @@ EXPORTS = ["nurbs_tables_bytes", "nurbs_tables", "nurbs_surface_fwd", "nurbs_sur
            "nurbs_surface_bwd_workspace_bytes", "nurbs_curve_fwd", "nurbs_curve_bwd",
            "nurbs_curve_bwd_workspace_bytes", "nurbs_validate", "nurbs_strerror",
            "nurbs_surface_fit_step", "nurbs_surface_fit_workspace_bytes", "nurbs_surface_derivs",
-           "nurbs_last_error_detail", "nurbs_abi_version"]
+           "nurbs_last_error_detail", "nurbs_abi_version", "nurbs_surface_points_fwd",
+           "nurbs_surface_points_bwd", "nurbs_surface_points_bwd_workspace_bytes", "nurbs_validate_points"]
 
 
 class nurbs_shape(ctypes.Structure):
@@ -64,6 +65,10 @@ def load() -> ctypes.CDLL:
         "nurbs_surface_fit_step": ([sh, P, P, P, P, P, P, P, ctypes.c_float, P, P, P, S, P], I),
         "nurbs_surface_fit_workspace_bytes": ([sh], S),
         "nurbs_surface_derivs": ([sh, P, P, P, P, P, P, P, P, P, P], I),
+        "nurbs_surface_points_fwd": ([sh, P, P, P, P, P, P], I),
+        "nurbs_surface_points_bwd": ([sh, P, P, P, P, P, P, P, P, P, S, P], I),
+        "nurbs_surface_points_bwd_workspace_bytes": ([sh], S),
+        "nurbs_validate_points": ([sh, P, P, P, P, P], I),
         "nurbs_strerror": ([I], ctypes.c_char_p),
         "nurbs_last_error_detail": ([], ctypes.c_char_p),
         "nurbs_abi_version": ([], I),

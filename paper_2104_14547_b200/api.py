@@ -131,6 +131,58 @@ def nurbs_validate(sh, ctrl, U, V, u, v, stream=None):
                                 _stream(stream)), "nurbs_validate")
 
 
+# ----------------------------------------------------------------------------- paired points (NEXT-1)
+def points_shape(ctrl: torch.Tensor, U: torch.Tensor, uv: torch.Tensor, p: int, q: int) -> nurbs_shape:
+    B, n, m, four = ctrl.shape
+    assert four == 4, "ctrl must be [B][n][m][4]"
+    assert uv.dim() == 3 and uv.shape[0] == B and uv.shape[2] == 2, "uv must be [B][N][2]"
+    return nurbs_shape(B, n, m, p, q, uv.shape[1], 1, 1 if U.dim() == 2 else 0)
+
+
+def points_workspace_bytes(sh: nurbs_shape) -> int:
+    return int(load().nurbs_surface_points_bwd_workspace_bytes(ctypes.byref(sh)))
+
+
+def nurbs_surface_points_fwd(sh, ctrl, U, V, uv, out, stream=None):
+    check(load().nurbs_surface_points_fwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(uv), _ptr(out),
+                                          _stream(stream)), "nurbs_surface_points_fwd")
+
+
+def nurbs_surface_points_bwd(sh, ctrl, U, V, uv, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes,
+                             stream=None):
+    check(load().nurbs_surface_points_bwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(uv),
+                                          _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U), _ptr(grad_V),
+                                          _ptr(workspace), ctypes.c_size_t(ws_bytes), _stream(stream)),
+          "nurbs_surface_points_bwd")
+
+
+def nurbs_validate_points(sh, ctrl, U, V, uv, stream=None):
+    check(load().nurbs_validate_points(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(uv), _stream(stream)),
+          "nurbs_validate_points")
+
+
+def surface_points_fwd(ctrl, U, V, uv, p: int, q: int, out=None, stream=None):
+    """S at paired points: out [B][N][3] for uv [B][N][2]."""
+    sh = points_shape(ctrl, U, uv, p, q)
+    if out is None:
+        out = torch.empty((sh.B, sh.n_u, 3), dtype=_F32, device=ctrl.device)
+    nurbs_surface_points_fwd(sh, ctrl, U, V, uv, out, stream)
+    return out
+
+
+def surface_points_bwd(ctrl, U, V, uv, grad_out, p: int, q: int, grad_ctrl=None, grad_U=None, grad_V=None,
+                       workspace=None, stream=None):
+    """dL/d(x,y,z,w) [B][n][m][4] at paired points (deterministic)."""
+    sh = points_shape(ctrl, U, uv, p, q)
+    if grad_ctrl is None:
+        grad_ctrl = torch.empty_like(ctrl)
+    ws = points_workspace_bytes(sh)
+    if workspace is None and ws > 0:
+        workspace = torch.empty(ws, dtype=torch.uint8, device=ctrl.device)
+    nurbs_surface_points_bwd(sh, ctrl, U, V, uv, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws, stream)
+    return grad_ctrl
+
+
 # ----------------------------------------------------------------------------- tables
 @dataclass
 class Tables:

@@ -27,9 +27,12 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17"] + ARCH + ["-Xcompiler", "-fPIC", "-di
 def units():
     u = [("nurbs_api", os.path.join(CSRC, "nurbs_api.cu"), []),
          ("nurbs_kernels", os.path.join(CSRC, "nurbs_kernels.cu"), []),
-         ("nurbs_derivs", os.path.join(CSRC, "nurbs_derivs.cu"), [])]
+         ("nurbs_derivs", os.path.join(CSRC, "nurbs_derivs.cu"), []),
+         ("nurbs_points", os.path.join(CSRC, "nurbs_points.cu"), [])]
     for p in range(6):
         u.append((f"nurbs_grid_p{p}", os.path.join(CSRC, "nurbs_grid_p.cu"), [f"-DNB_P={p}"]))
+    for p in range(1, 6):
+        u.append((f"nurbs_points_p{p}", os.path.join(CSRC, "nurbs_points_p.cu"), [f"-DNB_P={p}"]))
     return u
 
 

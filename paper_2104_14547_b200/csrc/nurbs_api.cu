@@ -11,6 +11,8 @@
 
 #include "../../include/nurbs.h"
 #include "nurbs_internal.cuh"
+#include "nurbs_points.cuh"
+#include "nurbs_points_plan.h"
 
 using nb::Dir;
 using nb::Params;
@@ -243,9 +245,145 @@ int check_ptrs(bool bwd, const void* ctrl, const void* out, const void* gout, co
   return NURBS_OK;
 }
 
+// ---- paired points (NEXT-1)
+int check_points_shape(const nurbs_shape* sh) {
+  if (!sh) return fail(NURBS_E_ARG, "shape is NULL");
+  if (sh->B < 0) return fail(NURBS_E_ARG, "negative batch %d", sh->B);
+  if (sh->knots_batched != 0 && sh->knots_batched != 1) return fail(NURBS_E_ARG, "knots_batched must be 0 or 1");
+  if (sh->n_v != 1) return fail(NURBS_E_ARG, "paired points need n_v = 1 (n_u = points per surface), got n_v=%d", sh->n_v);
+  int st = check_dir("u", sh->n, sh->p, sh->n_u);
+  if (st) return st;
+  return check_dir("v", sh->m, sh->q, 0);
+}
+
+nb::PtsParams points_params(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* uv) {
+  nb::PtsParams prm{};
+  prm.B = sh->B;
+  prm.n = sh->n;
+  prm.m = sh->m;
+  prm.N = sh->n_u;
+  prm.U = U;
+  prm.V = V;
+  prm.ustride = sh->knots_batched ? (long long)(sh->n + sh->p + 1) : 0LL;
+  prm.vstride = sh->knots_batched ? (long long)(sh->m + sh->q + 1) : 0LL;
+  prm.uv = reinterpret_cast<const float2*>(uv);
+  prm.ctrl = reinterpret_cast<const float4*>(ctrl);
+  return prm;
+}
+
+int validate_points(const nurbs_shape* sh, const nb::PtsParams& prm, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return cuda_fail(e, "validate_points: cudaMallocAsync");
+  e = cudaMemsetAsync(d, 0xff, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = nb::launch_points_validate(prm, sh->p, sh->q, d, st);
+  unsigned long long h = ~0ull;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(d, st);
+  if (e != cudaSuccess) return cuda_fail(e, "validate_points");
+  if (h == ~0ull) return NURBS_OK;
+  static const char* names[] = {"ctrl (weight <= 0 or non-finite)", "u knots", "v knots", "u of a point",
+                                "v of a point"};
+  const int which = (int)((h >> 40) & 0xff);
+  return fail((int)(h >> 48), "invalid %s at flat index %lld", which < 5 ? names[which] : "?",
+              (long long)(h & 0xffffffffffull));
+}
+
+int points_common(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* uv, bool bwd) {
+  if (!ctrl || !U || !V || !uv) return fail(NURBS_E_ARG, "NULL pointer");
+  if (!aligned16(ctrl)) return fail(NURBS_E_ARG, "ctrl must be 16-byte aligned (float4 control points)");
+  if ((reinterpret_cast<uintptr_t>(uv) & 7u) != 0) return fail(NURBS_E_ARG, "uv must be 8-byte aligned (float2 pairs)");
+  const nb::PtsPlan pl = nb::pts_plan(sh->B, sh->n, sh->m, sh->p, sh->q, sh->n_u);
+  if (!(bwd ? pl.fits_b : pl.fits_f))
+    return fail(NURBS_E_UNSUPPORTED, "paired points: %d x %d net (degrees %d, %d) exceeds the in-smem cell reduction",
+                sh->n, sh->m, sh->p, sh->q);
+  return NURBS_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+size_t nurbs_surface_points_bwd_workspace_bytes(const nurbs_shape* sh) {
+  if (!sh || sh->B <= 0 || sh->n_u <= 0 || sh->n <= sh->p || sh->m <= sh->q || sh->p < 1 || sh->q < 1) return 0;
+  return nb::pts_plan(sh->B, sh->n, sh->m, sh->p, sh->q, sh->n_u).ws_bytes;
+}
+
+int nurbs_validate_points(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* uv,
+                          void* stream) {
+  g_detail.clear();
+  int st = check_points_shape(sh);
+  if (st) return st;
+  if (!ctrl || !U || !V || (!uv && sh->n_u > 0 && sh->B > 0)) return fail(NURBS_E_ARG, "NULL pointer");
+  if (sh->B == 0) return NURBS_OK;
+  return validate_points(sh, points_params(sh, ctrl, U, V, uv), static_cast<cudaStream_t>(stream));
+}
+
+int nurbs_surface_points_fwd(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V,
+                             const float* uv, float* out, void* stream) {
+  g_detail.clear();
+  int st = check_points_shape(sh);
+  if (st) return st;
+  if (sh->B == 0 || sh->n_u == 0) return NURBS_OK;
+  if (!out) return fail(NURBS_E_ARG, "out is NULL");
+  if ((st = points_common(sh, ctrl, U, V, uv, false))) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  nb::PtsParams prm = points_params(sh, ctrl, U, V, uv);
+  if (check_mode() && (st = validate_points(sh, prm, s))) return st;
+  const nb::PtsPlan pl = nb::pts_plan(sh->B, sh->n, sh->m, sh->p, sh->q, sh->n_u);
+  if ((long long)sh->B * pl.nchunk_f > 0x7fffffffLL) return fail(NURBS_E_ARG, "too many points");
+  prm.out = out;
+  prm.chunk = pl.chunk_f;
+  prm.nchunk = pl.nchunk_f;
+  prm.ctrl_smem = pl.ctrl_smem;
+  cudaError_t e = nb::launch_points(prm, false, sh->p, sh->q, pl.smem_f, s);
+  return e == cudaSuccess ? NURBS_OK : cuda_fail(e, "paired forward kernel launch");
+}
+
+int nurbs_surface_points_bwd(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V,
+                             const float* uv, const float* grad_out, float* grad_ctrl, float* grad_U, float* grad_V,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  g_detail.clear();
+  int st = check_points_shape(sh);
+  if (st) return st;
+  if (sh->B == 0) return NURBS_OK;
+  if (!grad_ctrl) return fail(NURBS_E_ARG, "grad_ctrl is NULL");
+  if (!aligned16(grad_ctrl)) return fail(NURBS_E_ARG, "grad_ctrl must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int gU_n = (sh->n + sh->p + 1) * (sh->knots_batched ? sh->B : 1);
+  const int gV_n = (sh->m + sh->q + 1) * (sh->knots_batched ? sh->B : 1);
+  cudaError_t e = cudaSuccess;
+  if (grad_U) e = cudaMemsetAsync(grad_U, 0, sizeof(float) * (size_t)gU_n, s);
+  if (e == cudaSuccess && grad_V) e = cudaMemsetAsync(grad_V, 0, sizeof(float) * (size_t)gV_n, s);
+  if (e != cudaSuccess) return cuda_fail(e, "knot-gradient zero-fill");
+  if (sh->n_u == 0) {
+    e = cudaMemsetAsync(grad_ctrl, 0, (size_t)sh->B * sh->n * sh->m * 16, s);
+    return e == cudaSuccess ? NURBS_OK : cuda_fail(e, "zero-fill");
+  }
+  if (!grad_out) return fail(NURBS_E_ARG, "grad_out is NULL");
+  if ((st = points_common(sh, ctrl, U, V, uv, true))) return st;
+  nb::PtsParams prm = points_params(sh, ctrl, U, V, uv);
+  if (check_mode() && (st = validate_points(sh, prm, s))) return st;
+  const nb::PtsPlan pl = nb::pts_plan(sh->B, sh->n, sh->m, sh->p, sh->q, sh->n_u);
+  if ((long long)sh->B * pl.nchunk_b > 0x7fffffffLL) return fail(NURBS_E_ARG, "too many points");
+  if (pl.ws_bytes > 0 && (!workspace || ws_bytes < pl.ws_bytes))
+    return fail(NURBS_E_WORKSPACE, "paired backward needs a %zu-byte workspace (got %zu at %p)", pl.ws_bytes, ws_bytes,
+                workspace);
+  prm.gout = grad_out;
+  prm.gctrl = reinterpret_cast<float4*>(grad_ctrl);
+  prm.chunk = pl.chunk_b;
+  prm.nchunk = pl.nchunk_b;
+  prm.slots = pl.nchunk_b > 1 ? reinterpret_cast<float4*>(workspace) : nullptr;
+  e = nb::launch_points(prm, true, sh->p, sh->q, pl.smem_b, s);
+  if (e != cudaSuccess) return cuda_fail(e, "paired backward kernel launch");
+  if (pl.nchunk_b > 1) {
+    e = nb::launch_points_reduce(prm, s);
+    if (e != cudaSuccess) return cuda_fail(e, "paired reduce kernel launch");
+  }
+  return NURBS_OK;
+}
+
 
 int nurbs_abi_version(void) { return NURBS_ABI_VERSION; }
 
