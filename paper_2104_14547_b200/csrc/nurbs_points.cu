@@ -16,15 +16,16 @@ PtsPlan pts_plan(int B, int n, int m, int p, int q, int N) {
   PtsPlan pl{};
   const long long pts = (long long)B * N;
   const int ncell = (n - p) * (m - q);
-  // forward: ~16 CTAs per SM worth of points, chunks of 256..8192
-  long long cf = (pts + 148LL * 16 - 1) / (148LL * 16);
-  cf = (cf + 255) / 256 * 256;
-  if (cf < 256) cf = 256;
-  if (cf > 8192) cf = 8192;
-  pl.chunk_f = (int)(N < cf ? (N > 0 ? N : 1) : cf);
+  // forward: chunks of up to 4096 points (>= ~2 CTAs per SM when the batch is small)
+  long long cf = (pts + 148LL * 2 - 1) / (148LL * 2);
+  if (cf < 512) cf = 512;
+  if (cf > 4096) cf = 4096;
+  if (cf > N) cf = N > 0 ? N : 1;
+  while (cf > 64 && pts_fwd_layout(n, m, p, q, (int)cf).bytes > kPtsSmemMax) cf = (cf + 1) / 2;
+  pl.chunk_f = (int)cf;
   pl.nchunk_f = N > 0 ? (N + pl.chunk_f - 1) / pl.chunk_f : 0;
-  pl.ctrl_smem = (size_t)n * m * 16 <= 64 * 1024;
-  pl.smem_f = (pl.ctrl_smem ? (size_t)n * m * 16 : 0) + (size_t)pts_knots(n, m, p, q).floats * 4;
+  pl.ctrl_smem = 0;
+  pl.smem_f = pts_fwd_layout(n, m, p, q, pl.chunk_f).bytes;
   // backward: chunks of up to 8192 points (>= ~2 CTAs per SM when the batch is small), as
   // large as the smem budget allows
   long long cb = (pts + 148LL * 2 - 1) / (148LL * 2);
@@ -35,7 +36,7 @@ PtsPlan pts_plan(int B, int n, int m, int p, int q, int N) {
   pl.chunk_b = (int)cb;
   pl.nchunk_b = N > 0 ? (N + pl.chunk_b - 1) / pl.chunk_b : 0;
   pl.smem_b = pts_bwd_layout(n, m, p, q, pl.chunk_b).bytes;
-  pl.fits_f = pl.smem_f <= kPtsSmemMax;
+  pl.fits_f = ncell <= 65535 && pl.smem_f <= kPtsSmemMax;
   pl.fits_b = ncell <= 65535 && pl.smem_b <= kPtsSmemMax;
   pl.ws_bytes = pl.nchunk_b > 1 ? align_up((size_t)B * pl.nchunk_b * n * m * 16, 256) : 0;
   return pl;

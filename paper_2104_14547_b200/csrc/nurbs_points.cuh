@@ -49,47 +49,52 @@ struct PtsParams {
   int ctrl_smem;              // fwd: stage the homogeneous net in smem
 };
 
-// ---- smem layout of the per-CTA knot data: U, V, then the reciprocal tables (R23)
+// ---- smem layout of the per-CTA knot data: U, V (for FindSpan), then one record per knot
+// span and direction: rec[0..2p) = U[s-p+1 .. s+p] (the knots A2.2 reads) and
+// rec[2p + tri(j-1) + r] = 1 / (U[s+r+1] - U[s+r+1-j]) (R23), padded to a float4 multiple.
+__host__ __device__ constexpr int rec_len(int p) { return (2 * p + tri(p) + 3) / 4 * 4; }
 struct PtsKnots {
-  int offV, offIU, offIV, floats;
+  int offV, offRU, offRV, floats;
 };
 __host__ __device__ inline PtsKnots pts_knots(int n, int m, int p, int q) {
   PtsKnots k;
   k.offV = n + p + 1;
-  k.offIU = k.offV + m + q + 1;
-  k.offIV = k.offIU + (n - p) * tri(p);
-  k.floats = k.offIV + (m - q) * tri(q);
+  k.offRU = (k.offV + m + q + 1 + 3) / 4 * 4;
+  k.offRV = k.offRU + (n - p) * rec_len(p);
+  k.floats = k.offRV + (m - q) * rec_len(q);
   return k;
 }
 
-// FindSpan (R2-R4) over knots in smem: largest s in [p, n-1] with U[s] <= u, stepped
-// down over empty intervals (only possible at u == U[n]); out-of-domain u is clamped (the
-// checked mode rejects it). Plain fp32 comparisons: bit-exact with the oracle.
-__device__ __forceinline__ int s_find_span(const float* U, int n, int p, float u) {
-  if (!(u >= U[p])) return p;
-  int lo = p, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (U[mid] <= u) lo = mid; else hi = mid - 1;
-  }
-  while (lo > p && U[lo] == U[lo + 1]) --lo;
-  return lo;
+// FindSpan (R2-R4) over knots in smem: the largest s in [p, n-1] with U[s] <= u,
+// stepped down over empty intervals (only possible at u == U[n]); out-of-domain u is clamped
+// (the checked mode rejects it). The walk starts from the uniform-knot guess
+// p + floor((u - U[p]) (n-p) / (U[n] - U[p])) and moves until U[s] <= u < U[s+1], so the
+// result is the exact A2.1 span for any knots (one or two compares for near-uniform ones).
+// Plain fp32 comparisons: bit-exact with the oracle.
+__device__ __forceinline__ int s_find_span(const float* U, int n, int p, float u, float u0, float scale) {
+  const float t = fminf(fmaxf((u - u0) * scale, 0.f), (float)(n - p - 1));
+  int s = p + (int)t;
+  const float a = U[s], b = U[s + 1];
+  if (a <= u && u < b) return s;  // the guess (exact for uniform knots away from the end)
+  while (s < n - 1 && U[s + 1] <= u) ++s;
+  while (s > p && U[s] > u) --s;
+  while (s > p && U[s] == U[s + 1]) --s;
+  return s;
 }
 
-// A2.2 (Eq.4) with the tabulated reciprocal denominators of span s:
-// inv[tri(j-1) + r] = 1 / (U[s+r+1] - U[s+r+1-j]).
-template <int P>
-__device__ __forceinline__ void basis_inv(const float* U, const float* inv, int s, float u, float (&N)[P + 1]) {
+// A2.2 (Eq.4) from a span record (registers or smem).
+template <int P, typename R>
+__device__ __forceinline__ void basis_rec(const R& rec, float u, float (&N)[P + 1]) {
   float left[P + 1], right[P + 1];
   N[0] = 1.f;
 #pragma unroll
   for (int j = 1; j <= P; ++j) {
-    left[j] = u - U[s + 1 - j];
-    right[j] = U[s + j] - u;
+    left[j] = u - rec[P - j];         // u - U[s+1-j]
+    right[j] = rec[P - 1 + j] - u;    // U[s+j] - u
     float saved = 0.f;
 #pragma unroll
     for (int r = 0; r < j; ++r) {
-      const float temp = N[r] * inv[tri(j - 1) + r];
+      const float temp = N[r] * rec[2 * P + tri(j - 1) + r];
       N[r] = fmaf(right[r + 1], temp, saved);
       saved = left[j - r] * temp;
     }
@@ -97,78 +102,258 @@ __device__ __forceinline__ void basis_inv(const float* U, const float* inv, int 
   }
 }
 
-// Knots of surface s and the reciprocal tables into smem (all threads; ends with a barrier).
+template <int P>
+__device__ __forceinline__ void load_rec(const float* src, float (&rec)[rec_len(P)]) {
+#pragma unroll
+  for (int k = 0; k < rec_len(P); k += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(src + k);
+    rec[k] = v.x; rec[k + 1] = v.y; rec[k + 2] = v.z; rec[k + 3] = v.w;
+  }
+}
+
+// Knots of surface s and the span records into smem (all threads; ends with a barrier).
 template <int P, int Q>
 __device__ __forceinline__ void pts_stage_knots(const PtsParams& prm, int s, float* ks) {
   const int n = prm.n, m = prm.m;
   const PtsKnots L = pts_knots(n, m, P, Q);
   const float* Uk = prm.U + (long long)s * prm.ustride;
   const float* Vk = prm.V + (long long)s * prm.vstride;
-  for (int i = threadIdx.x; i < L.offIU; i += blockDim.x)
+  for (int i = threadIdx.x; i < L.offV + m + Q + 1; i += blockDim.x)
     ks[i] = i < L.offV ? __ldg(Uk + i) : __ldg(Vk + i - L.offV);
   __syncthreads();
-  const int nU = (n - P) * tri(P), nV = (m - Q) * tri(Q);
+  constexpr int RU = rec_len(P), RV = rec_len(Q);
+  const int nU = (n - P) * RU, nV = (m - Q) * RV;
   for (int e = threadIdx.x; e < nU + nV; e += blockDim.x) {
     const bool isU = e < nU;
-    const int p = isU ? P : Q;
+    const int p = isU ? P : Q, R = isU ? RU : RV;
     const int k = isU ? e : e - nU;
-    const int t = tri(p);
-    const int s_ = k / t + p, idx = k - (k / t) * t;
-    int j = 1;
-    while (tri(j) <= idx) ++j;             // idx = tri(j-1) + r
-    const int r = idx - tri(j - 1);
+    const int sp = k / R + p, idx = k - (k / R) * R;
     const float* K = isU ? ks : ks + L.offV;
-    const float d = K[s_ + r + 1] - K[s_ + r + 1 - j];
-    ks[(isU ? L.offIU : L.offIV) + k] = d > 0.f ? 1.f / d : 0.f;  // empty spans are never used
+    float val = 0.f;
+    if (idx < 2 * p) {
+      val = K[sp - p + 1 + idx];
+    } else if (idx < 2 * p + tri(p)) {
+      const int t = idx - 2 * p;
+      int j = 1;
+      while (tri(j) <= t) ++j;            // t = tri(j-1) + r
+      const int r = t - tri(j - 1);
+      const float d = K[sp + r + 1] - K[sp + r + 1 - j];
+      val = d > 0.f ? 1.f / d : 0.f;      // empty spans are never selected
+    }
+    ks[(isU ? L.offRU : L.offRV) + k] = val;
   }
   __syncthreads();
 }
 
-// ------------------------------------------------------------------------ forward
+// Pass 2 of the sorts: cstart[c] = exclusive prefix over cells of the NW per-row counts
+// hist[w][c]; each count is replaced by its row's cursor (cell-major, then row order).
+template <int NW>
+__device__ __forceinline__ void pts_scan(int* hist, int* cstart, int C, int cnt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int seg = (C + kPtsThreads - 1) / kPtsThreads;
+  const int c0 = min(C, tid * seg), c1 = min(C, c0 + seg);
+  int sum = 0;
+  for (int ce = c0; ce < c1; ++ce)
+#pragma unroll
+    for (int w = 0; w < NW; ++w) sum += hist[w * (C + 1) + ce];
+  int incl = sum;  // block-wide inclusive scan of the per-thread sums
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __shared__ int wsum[kPtsWarps];
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  int run = base + incl - sum;
+  for (int ce = c0; ce < c1; ++ce) {
+    cstart[ce] = run;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int h = hist[w * (C + 1) + ce];
+      hist[w * (C + 1) + ce] = run;
+      run += h;
+    }
+  }
+  if (tid == kPtsThreads - 1) cstart[C] = cnt;
+  __syncthreads();
+}
+
+// Passes 1-3 of the backward: STABLE in-smem counting sort of a chunk's cnt points by knot
+// cell (su - p, sv - q). On return (after a barrier): cstart[c] .. cstart[c+1] index the
+// points of cell c in sorted[], in (warp slice, position) order — a function of the input
+// only (smem integer atomics from one warp execute in program order). hist
+// [kPtsWarps][C+1] must be zero on entry. uv may be global or shared memory.
 template <int P, int Q>
-__global__ void __launch_bounds__(kPtsThreads) nurbs_points_fwd_kernel(PtsParams prm) {
+__device__ __forceinline__ void pts_sort(const float2* uv, int cnt, int n, int m, const float* Us, const float* Vs,
+                                         int* hist, int* cstart, unsigned short* cell, unsigned short* sorted) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Cv = m - Q, C = (n - P) * Cv;
+  const float u0 = Us[P], su_scale = (float)(n - P) / (Us[n] - Us[P]);
+  const float v0 = Vs[Q], sv_scale = (float)(m - Q) / (Vs[m] - Vs[Q]);
+  // ---- pass 1: cell of every point; per-warp counts over the warp's contiguous slice
+  const int per_warp = (cnt + kPtsWarps - 1) / kPtsWarps;
+  const int w0 = warp * per_warp, w1 = min(cnt, w0 + per_warp);
+  int* hw = hist + warp * (C + 1);
+  float2 xn = (w0 + lane < w1) ? uv[w0 + lane] : make_float2(0.f, 0.f);
+  for (int b = w0; b < w1; b += 32) {
+    const int i = b + lane;
+    const float2 x = xn;
+    if (b + 32 + lane < w1) xn = uv[b + 32 + lane];  // next tile in flight
+    int ce = C;  // sentinel for lanes past the slice
+    if (i < w1) {
+      const int su = s_find_span(Us, n, P, x.x, u0, su_scale);
+      const int sv = s_find_span(Vs, m, Q, x.y, v0, sv_scale);
+      ce = (su - P) * Cv + (sv - Q);
+      cell[i] = (unsigned short)ce;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, ce);
+    if (ce < C && lane == __ffs(peers) - 1) atomicAdd(hw + ce, __popc(peers));  // no return: RED
+  }
+  __syncthreads();
+  pts_scan<kPtsWarps>(hist, cstart, C, cnt);
+  // ---- pass 3: stable scatter (cell, warp, position in the warp's slice)
+  for (int b = w0; b < w1; b += 32) {
+    const int i = b + lane;
+    const int ce = i < w1 ? (int)cell[i] : C;
+    const unsigned peers = __match_any_sync(0xffffffffu, ce);
+    const int leader = __ffs(peers) - 1;
+    int pos = 0;
+    if (ce < C && lane == leader) pos = atomicAdd(hw + ce, __popc(peers));
+    pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+    if (ce < C) sorted[pos] = (unsigned short)i;
+  }
+  __syncthreads();
+}
+
+// Passes 1-3 of the forward: the same bucketing without the stability (every point's result
+// is independent of the order): one count per cell, smem atomics, any order within a cell.
+template <int P, int Q>
+__device__ __forceinline__ void pts_bucket(const float2* uv, int cnt, int n, int m, const float* Us, const float* Vs,
+                                           int* hist, int* cstart, unsigned short* cell, unsigned short* sorted) {
+  const int tid = threadIdx.x;
+  const int Cv = m - Q, C = (n - P) * Cv;
+  const float u0 = Us[P], su_scale = (float)(n - P) / (Us[n] - Us[P]);
+  const float v0 = Vs[Q], sv_scale = (float)(m - Q) / (Vs[m] - Vs[Q]);
+  for (int i = tid; i < cnt; i += kPtsThreads) {
+    const float2 x = uv[i];
+    const int su = s_find_span(Us, n, P, x.x, u0, su_scale);
+    const int sv = s_find_span(Vs, m, Q, x.y, v0, sv_scale);
+    const int ce = (su - P) * Cv + (sv - Q);
+    cell[i] = (unsigned short)ce;
+    atomicAdd(hist + ce, 1);
+  }
+  __syncthreads();
+  pts_scan<1>(hist, cstart, C, cnt);
+  for (int i = tid; i < cnt; i += kPtsThreads) sorted[atomicAdd(hist + cell[i], 1)] = (unsigned short)i;
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------ forward
+// CTA = (surface, chunk of points). The chunk's (u, v) are staged in smem, bucketed by knot
+// cell (pts_bucket), then groups of kGrpF lanes own cells: the cell's homogeneous control points
+// and span records sit in registers, so each point costs its basis and 4(p+1)(q+1+1)
+// register FMAs — no per-point gather of control points from smem (which would be
+// bank-conflicted random 16-byte loads). Results go to an smem copy of the chunk's output,
+// written to HBM coalesced at the end.
+constexpr int kGrpF = 4;
+struct PtsFwdLayout {
+  size_t uv, outs, cstart, hist, cell, sorted, knots, bytes;
+};
+__host__ __device__ inline PtsFwdLayout pts_fwd_layout(int n, int m, int p, int q, int chunk) {
+  PtsFwdLayout L;
+  const int C = (n - p) * (m - q);
+  size_t o = 0;
+  L.uv = o;     o += ((size_t)chunk * 8 + 15) & ~(size_t)15;
+  L.outs = o;   o += (size_t)chunk * 12;
+  o = (o + 15) & ~(size_t)15;
+  L.cstart = o; o += (size_t)(C + 1) * 4;
+  L.hist = o;   o += (size_t)(C + 1) * 4;
+  L.cell = o;   o += (size_t)chunk * 2;
+  L.sorted = o; o += (size_t)chunk * 2;
+  o = (o + 15) & ~(size_t)15;
+  L.knots = o;  o += (size_t)pts_knots(n, m, p, q).floats * 4;
+  L.bytes = (o + 15) & ~(size_t)15;
+  return L;
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_fwd_kernel(PtsParams prm) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int RU = rec_len(P), RV = rec_len(Q);
+  constexpr int GPW = 32 / kGrpF, NG = kPtsWarps * GPW;
   const int s = blockIdx.x / prm.nchunk;
   const int c = blockIdx.x - s * prm.nchunk;
   const int n = prm.n, m = prm.m;
-  const PtsKnots L = pts_knots(n, m, P, Q);
-  float4* Qs = reinterpret_cast<float4*>(smem);                               // [n*m] (ctrl_smem)
-  float* ks = reinterpret_cast<float*>(smem + (prm.ctrl_smem ? (size_t)n * m * 16 : 0));
-  const float4* ctrl_s = prm.ctrl + (size_t)s * n * m;
-  if (prm.ctrl_smem)
-    for (int i = threadIdx.x; i < n * m; i += kPtsThreads) Qs[i] = homog(__ldg(ctrl_s + i));
-  pts_stage_knots<P, Q>(prm, s, ks);
-  const float* Us = ks;
-  const float* Vs = ks + L.offV;
+  const int Cv = m - Q, C = (n - P) * Cv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const PtsFwdLayout SL = pts_fwd_layout(n, m, P, Q, prm.chunk);
+  const PtsKnots KL = pts_knots(n, m, P, Q);
+  float2* uvs = reinterpret_cast<float2*>(smem + SL.uv);
+  float* outs = reinterpret_cast<float*>(smem + SL.outs);
+  int* cstart = reinterpret_cast<int*>(smem + SL.cstart);
+  int* hist = reinterpret_cast<int*>(smem + SL.hist);
+  unsigned short* cell = reinterpret_cast<unsigned short*>(smem + SL.cell);
+  unsigned short* sorted = reinterpret_cast<unsigned short*>(smem + SL.sorted);
+  float* ks = reinterpret_cast<float*>(smem + SL.knots);
   const int t0 = c * prm.chunk;
   const int cnt = min(prm.chunk, prm.N - t0);
   const float2* uv = prm.uv + (size_t)s * prm.N + t0;
-  float* out = prm.out + ((size_t)s * prm.N + t0) * 3;
-  for (int i = threadIdx.x; i < cnt; i += kPtsThreads) {
-    const float2 x = __ldg(uv + i);
-    const int su = s_find_span(Us, n, P, x.x);
-    const int sv = s_find_span(Vs, m, Q, x.y);
-    float Nu[P + 1], Nv[Q + 1];
-    basis_inv<P>(Us, ks + L.offIU + (su - P) * tri(P), su, x.x, Nu);
-    basis_inv<Q>(Vs, ks + L.offIV + (sv - Q) * tri(Q), sv, x.y, Nv);
-    float4 Sp = f4(0.f);
+  for (int i = tid; i < cnt; i += kPtsThreads) uvs[i] = __ldg(uv + i);
+  for (int i = tid; i <= C; i += kPtsThreads) hist[i] = 0;
+  pts_stage_knots<P, Q>(prm, s, ks);  // ends with __syncthreads
+  const float* Us = ks;
+  const float* Vs = ks + KL.offV;
+  pts_bucket<P, Q>(uvs, cnt, n, m, Us, Vs, hist, cstart, cell, sorted);
+
+  const float4* ctrl_s = prm.ctrl + (size_t)s * n * m;
+  const int grp = lane / kGrpF, gl = lane - grp * kGrpF;
+  const int G = warp * GPW + grp;
+  const int nsteps = (C - warp * GPW + NG - 1) / NG;
+  for (int k = 0; k < nsteps; ++k) {
+    const int ce = G + k * NG;
+    const bool has = ce < C;
+    const int beg = has ? cstart[ce] : 0, end = has ? cstart[ce + 1] : 0;
+    if (end <= beg) continue;  // no shuffles below: groups may diverge freely
+    const int cu = ce / Cv, cv = ce - cu * Cv;
+    float4 Qc[P + 1][Q + 1];   // the cell's homogeneous control points
 #pragma unroll
-    for (int r = 0; r <= P; ++r) {
-      const int row = (su - P + r) * m + (sv - Q);
-      float4 T = f4(0.f);
-      if (prm.ctrl_smem) {
+    for (int r = 0; r <= P; ++r)
 #pragma unroll
-        for (int h = 0; h <= Q; ++h) T = fma4v(Nv[h], Qs[row + h], T);
-      } else {
+      for (int h = 0; h <= Q; ++h) Qc[r][h] = homog(__ldg(ctrl_s + (cu + r) * m + cv + h));
+    float ru[RU];  // u record in registers; the v record is read from smem (register budget)
+    load_rec<P>(ks + KL.offRU + cu * RU, ru);
+    const float* rv = ks + KL.offRV + cv * RV;
+    for (int kk = beg + gl; kk < end; kk += kGrpF) {
+      const int i = sorted[kk];
+      const float2 x = uvs[i];
+      float Nu[P + 1], Nv[Q + 1];
+      basis_rec<P>(ru, x.x, Nu);
+      basis_rec<Q>(rv, x.y, Nv);
+      float4 Sp = f4(0.f);
 #pragma unroll
-        for (int h = 0; h <= Q; ++h) T = fma4v(Nv[h], homog(__ldg(ctrl_s + row + h)), T);
+      for (int r = 0; r <= P; ++r) {
+        float4 T = f4(0.f);
+#pragma unroll
+        for (int h = 0; h <= Q; ++h) T = fma4v(Nv[h], Qc[r][h], T);
+        Sp = fma4v(Nu[r], T, Sp);
       }
-      Sp = fma4v(Nu[r], T, Sp);
+      const float rw = rcp_approx(Sp.w);
+      outs[3 * i + 0] = Sp.x * rw;
+      outs[3 * i + 1] = Sp.y * rw;
+      outs[3 * i + 2] = Sp.z * rw;
     }
-    const float rw = 1.f / Sp.w;
-    out[3 * i + 0] = Sp.x * rw;
-    out[3 * i + 1] = Sp.y * rw;
-    out[3 * i + 2] = Sp.z * rw;
+  }
+  __syncthreads();
+  float* out = prm.out + ((size_t)s * prm.N + t0) * 3;
+  if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+    const int n4 = (cnt * 3) / 4;
+    for (int i = tid; i < n4; i += kPtsThreads) reinterpret_cast<float4*>(out)[i] = reinterpret_cast<const float4*>(outs)[i];
+    for (int i = 4 * n4 + tid; i < cnt * 3; i += kPtsThreads) out[i] = outs[i];
+  } else {
+    for (int i = tid; i < cnt * 3; i += kPtsThreads) out[i] = outs[i];
   }
 }
 
@@ -198,7 +383,7 @@ __host__ __device__ inline PtsBwdLayout pts_bwd_layout(int n, int m, int p, int 
   const int C = (n - p) * (m - q);
   size_t o = 0;
   L.dq = o;     o += (size_t)kPtsWarps * n * m * 16;                 // per-warp dQ copies
-  L.cq = o;     o += (size_t)kGroups * (p + 1) * (q + 1) * 16;      // per-group cell net
+  L.cq = o;     o += (size_t)kGroups * ((p + 1) * (q + 1) + 1) * 16;  // per-group cell net (+16 B: banks)
   L.cstart = o; o += (size_t)(C + 1) * 4;                            // cell start offsets
   L.hist = o;   o += (size_t)kPtsWarps * (C + 1) * 4;                // per-warp counts / cursors
   L.cell = o;   o += (size_t)chunk * 2;                              // cell of point i (uint16)
@@ -242,98 +427,49 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_bwd_kernel(PtsPar
   const float* g = prm.gout + ((size_t)s * prm.N + t0) * 3;
   const float4* ctrl_s = prm.ctrl + (size_t)s * nm;
 
-  // ---- pass 1: cell of every point; per-warp counts over the warp's contiguous slice
-  const int per_warp = (cnt + kPtsWarps - 1) / kPtsWarps;
-  const int w0 = warp * per_warp, w1 = min(cnt, w0 + per_warp);
-  int* hw = hist + warp * (C + 1);
-  for (int b = w0; b < w1; b += 32) {
-    const int i = b + lane;
-    int ce = C;  // sentinel for lanes past the slice
-    if (i < w1) {
-      const float2 x = __ldg(uv + i);
-      const int su = s_find_span(Us, n, P, x.x);
-      const int sv = s_find_span(Vs, m, Q, x.y);
-      ce = (su - P) * Cv + (sv - Q);
-      cell[i] = (unsigned short)ce;
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, ce);
-    if (ce < C && lane == __ffs(peers) - 1) hw[ce] += __popc(peers);
-  }
-  __syncthreads();
-
-  // ---- pass 2: cell starts (exclusive scan over cells) and per-warp cursors
-  {
-    const int seg = (C + kPtsThreads - 1) / kPtsThreads;
-    const int c0 = min(C, tid * seg), c1 = min(C, c0 + seg);
-    int sum = 0;
-    for (int ce = c0; ce < c1; ++ce)
-      for (int w = 0; w < kPtsWarps; ++w) sum += hist[w * (C + 1) + ce];
-    int incl = sum;  // block-wide inclusive scan of the per-thread sums
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    __shared__ int wsum[kPtsWarps];
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    int base = 0;
-    for (int w = 0; w < warp; ++w) base += wsum[w];
-    int run = base + incl - sum;
-    for (int ce = c0; ce < c1; ++ce) {
-      cstart[ce] = run;
-      for (int w = 0; w < kPtsWarps; ++w) {
-        const int h = hist[w * (C + 1) + ce];
-        hist[w * (C + 1) + ce] = run;
-        run += h;
-      }
-    }
-    if (tid == kPtsThreads - 1) cstart[C] = cnt;
-  }
-  __syncthreads();
-
-  // ---- pass 3: stable scatter (cell, warp, position in the warp's slice)
-  for (int b = w0; b < w1; b += 32) {
-    const int i = b + lane;
-    const int ce = i < w1 ? (int)cell[i] : C;
-    const unsigned peers = __match_any_sync(0xffffffffu, ce);
-    const int rank = __popc(peers & ((1u << lane) - 1u));
-    if (ce < C) sorted[hw[ce] + rank] = (unsigned short)i;
-    __syncwarp();
-    if (ce < C && lane == __ffs(peers) - 1) hw[ce] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
+  // ---- passes 1-3: stable counting sort of the chunk's points by knot cell
+  pts_sort<P, Q>(uv, cnt, n, m, Us, Vs, hist, cstart, cell, sorted);
 
   // ---- pass 4: groups of kGrp lanes own cells; warp w's groups take cells w*4+g (+32 k)
   const int grp = lane / kGrp, gl = lane - grp * kGrp;
   const int G = warp * kGrpPerWarp + grp;
-  float4* cqg = cq + G * NC;
+  float4* cqg = cq + G * (NC + 1);
   float4* dq = dqw + warp * nm;
+  constexpr int RU = rec_len(P), RV = rec_len(Q);
   const int nsteps = (C - warp * kGrpPerWarp + kGroups - 1) / kGroups;
   for (int k = 0; k < nsteps; ++k) {
     const int ce = G + k * kGroups;
     const bool has = ce < C;
     const int beg = has ? cstart[ce] : 0, end = has ? cstart[ce + 1] : 0;
     const int cu = has ? ce / Cv : 0, cv = has ? ce - cu * Cv : 0;
-    const int su = cu + P, sv = cv + Q;
     if (has && end > beg)  // the cell's homogeneous control points -> smem
       for (int e = gl; e < NC; e += kGrp) {
         const int r = e / (Q + 1), h = e - r * (Q + 1);
         cqg[e] = homog(__ldg(ctrl_s + (cu + r) * m + cv + h));
       }
     __syncwarp();
+    float ru[RU], rv[RV];  // the cell's span records, in registers for all its points
+    load_rec<P>(ks + KL.offRU + cu * RU, ru);
+    load_rec<Q>(ks + KL.offRV + cv * RV, rv);
     float acc[NPAD];
 #pragma unroll
     for (int e = 0; e < NPAD; ++e) acc[e] = 0.f;
-    const float* iU = ks + KL.offIU + cu * tri(P);
-    const float* iV = ks + KL.offIV + cv * tri(Q);
-    for (int kk = beg + gl; kk < end; kk += kGrp) {
-      const int i = sorted[kk];
-      const float2 x = __ldg(uv + i);
+    int kk = beg + gl;
+    int in = kk < end ? sorted[kk] : 0;
+    float2 xn = kk < end ? __ldg(uv + in) : make_float2(0.f, 0.f);
+    float g0n = kk < end ? __ldg(g + 3 * in) : 0.f, g1n = kk < end ? __ldg(g + 3 * in + 1) : 0.f,
+          g2n = kk < end ? __ldg(g + 3 * in + 2) : 0.f;
+    for (; kk < end; kk += kGrp) {
+      const float2 x = xn;
+      const float g0 = g0n, g1 = g1n, g2 = g2n;
+      if (kk + kGrp < end) {  // next point of this lane in flight
+        in = sorted[kk + kGrp];
+        xn = __ldg(uv + in);
+        g0n = __ldg(g + 3 * in); g1n = __ldg(g + 3 * in + 1); g2n = __ldg(g + 3 * in + 2);
+      }
       float Nu[P + 1], Nv[Q + 1];
-      basis_inv<P>(Us, iU, su, x.x, Nu);
-      basis_inv<Q>(Vs, iV, sv, x.y, Nv);
+      basis_rec<P>(ru, x.x, Nu);
+      basis_rec<Q>(rv, x.y, Nv);
       float4 Sp = f4(0.f);
 #pragma unroll
       for (int r = 0; r <= P; ++r) {
@@ -342,8 +478,8 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_bwd_kernel(PtsPar
         for (int h = 0; h <= Q; ++h) T = fma4v(Nv[h], cqg[r * (Q + 1) + h], T);
         Sp = fma4v(Nu[r], T, Sp);
       }
-      const float rw = 1.f / Sp.w;
-      const float gx = __ldg(g + 3 * i) * rw, gy = __ldg(g + 3 * i + 1) * rw, gz = __ldg(g + 3 * i + 2) * rw;
+      const float rw = rcp_approx(Sp.w);
+      const float gx = g0 * rw, gy = g1 * rw, gz = g2 * rw;
       const float gS = fmaf(gx, Sp.x, fmaf(gy, Sp.y, gz * Sp.z));
       const float4 Gh = make_float4(gx, gy, gz, -gS * rw);   // G = (g/W, -(g.S)/W)
 #pragma unroll
