@@ -393,20 +393,16 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     b2a.lps = L;
     b2a.fast = b2fast; b2a.direct = prm.direct; b2a.band_in_smem = band_in_smem;
   }
+  // One generic pointer + stride for both sources (the staged band in smem, or the net in
+  // global memory when the block's columns do not fit the band): a uniform select once per
+  // CTA instead of two predicated load paths in every unrolled window advance.
+  const float4* tb0 = band_in_smem ? cb0 : cg0;
+  const size_t tstride = band_in_smem ? (size_t)prm.CBW : (size_t)m;
   auto Trow = [&](int i) -> float4 {
-    float4 c[Q + 1];
-    if (band_in_smem) {
-      const float4* src = cb0 + (size_t)i * prm.CBW;
-#pragma unroll
-      for (int h = 0; h <= Q; ++h) c[h] = src[h];
-    } else {
-      const float4* src = cg0 + (size_t)i * m;
-#pragma unroll
-      for (int h = 0; h <= Q; ++h) c[h] = __ldg(src + h);
-    }
+    const float4* src = tb0 + (size_t)i * tstride;
     float4 a = f4(0.f);
 #pragma unroll
-    for (int h = 0; h <= Q; ++h) a = fma4v(nv[h], homog(c[h]), a);
+    for (int h = 0; h <= Q; ++h) a = fma4v(nv[h], homog(src[h]), a);
     return a;
   };
 
