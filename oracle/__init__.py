@@ -59,6 +59,10 @@ def lib():
         pts = [c_int] * 7 + [d, d, d, d]
         L.nurbs_ref_surface_fwd_points.argtypes = pts + [d]
         L.nurbs_ref_surface_bwd_points.argtypes = pts + [d, d]
+        L.nurbs_ref_basis_dknot.argtypes = [c_int, c_int, d, ctypes.c_double, c_int, d]
+        L.nurbs_ref_basis_dknot.restype = None
+        L.nurbs_ref_surface_knot_grad.argtypes = surf + [d, d, d]
+        L.nurbs_ref_curve_knot_grad.argtypes = [c_int] * 5 + [d, d, d, d, d]
         L.nurbs_ref_curve_fwd.argtypes = [c_int] * 5 + [d, d, d, d]
         L.nurbs_ref_curve_bwd.argtypes = [c_int] * 5 + [d, d, d, d, d]
         _lib = L
@@ -212,6 +216,35 @@ def surface_bwd_points(ctrl, U, V, uv, gout, p: int, q: int, knots_batched: bool
     _chk(lib().nurbs_ref_surface_bwd_points(*dims, _p(ctrl), _p(U), _p(V), _p(uv), _p(g), _p(grad)),
          "bwd_points")
     return grad
+
+
+def basis_dknot(n: int, p: int, U, u: float, kk: int) -> np.ndarray:
+    """dN_{i,p}(u)/dU[kk] for i = 0..n-1 (NEXT-4; Eq.4 differentiated)."""
+    U = _d(U)
+    dN = np.zeros(n)
+    lib().nurbs_ref_basis_dknot(n, p, _p(U), float(u), int(kk), _p(dN))
+    return dN
+
+
+def surface_knot_grad(ctrl, U, V, u, v, gout, p: int, q: int, knots_batched: bool = False):
+    """(dL/dU, dL/dV): [(B if batched else 1)][n+p+1], [..][m+q+1] (NEXT-4)."""
+    ctrl, U, V, u, v, dims = _surf_args(ctrl, U, V, u, v, p, q, knots_batched)
+    B, n, m = dims[:3]
+    g = _d(gout)
+    nb_ = B if knots_batched else 1
+    gU, gV = np.zeros((nb_, n + p + 1)), np.zeros((nb_, m + q + 1))
+    _chk(lib().nurbs_ref_surface_knot_grad(*dims, _p(ctrl), _p(U), _p(V), _p(u), _p(v), _p(g), _p(gU), _p(gV)),
+         "surface_knot_grad")
+    return gU, gV
+
+
+def curve_knot_grad(ctrl, U, u, gout, p: int, knots_batched: bool = False) -> np.ndarray:
+    ctrl, U, u, g = _d(ctrl), _d(U), _d(u), _d(gout)
+    B, n, _ = ctrl.shape
+    gU = np.zeros((B if knots_batched else 1, n + p + 1))
+    _chk(lib().nurbs_ref_curve_knot_grad(B, n, p, len(u), int(knots_batched), _p(ctrl), _p(U), _p(u), _p(g),
+                                         _p(gU)), "curve_knot_grad")
+    return gU
 
 
 def curve_fwd(ctrl, U, u, p: int, knots_batched: bool = False) -> np.ndarray:

@@ -727,3 +727,167 @@ int nurbs_ref_surface_bwd_points(int B, int n, int m, int p, int q, int N, int k
     }
     return REF_OK;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-4: true knot gradients (the paper sets them to zero, §3.2.2; this extension */
+/* is "parity pinned by FD alone" plus two exact invariants).              */
+/* dN_{i,p}(u)/dU[kk] for all i (dense), by differentiating the recursion Eq.4   */
+/* with the quotient rule; Eq.5's degree-0 functions are piecewise constant, so their     */
+/* knot derivative is 0 (u is never at an interval end the derivative is taken at). With  */
+/*   N_{i,k} = a N_{i,k-1} + b N_{i+1,k-1},                                               */
+/*   a = (u - U_i)/(U_{i+k} - U_i),  b = (U_{i+k+1} - u)/(U_{i+k+1} - U_{i+1})  (0/0 := 0): */
+/*   da/dU_i = (u - U_{i+k})/d1^2,   da/dU_{i+k} = -(u - U_i)/d1^2,                        */
+/*   db/dU_{i+1} = (U_{i+k+1} - u)/d2^2,  db/dU_{i+k+1} = (u - U_{i+1})/d2^2.             */
+/* dN_out[0..n-1].                                                                       */
+/* ------------------------------------------------------------------------------------ */
+void nurbs_ref_basis_dknot(int n, int p, const double* U, double u, int kk, double* dN_out)
+{
+    int nk = n + p + 1, n0 = nk - 1;
+    double* N = (double*)calloc((size_t)n0, sizeof(double));
+    double* D = (double*)calloc((size_t)n0, sizeof(double));
+    if (u == U[n]) {
+        int s = n - 1;
+        while (s > p && U[s] == U[s + 1]) --s;
+        N[s] = 1.0;
+    } else {
+        for (int i = 0; i < n0; ++i) N[i] = (U[i] <= u && u < U[i + 1]) ? 1.0 : 0.0;
+    }
+    for (int k = 1; k <= p; ++k) {
+        for (int i = 0; i < n0 - k; ++i) {
+            double d1 = U[i + k] - U[i], d2 = U[i + k + 1] - U[i + 1];
+            double a = 0.0, da = 0.0, b = 0.0, db = 0.0;
+            if (d1 != 0.0) {
+                a = (u - U[i]) / d1;
+                if (kk == i) da += (u - U[i + k]) / (d1 * d1);
+                if (kk == i + k) da += -(u - U[i]) / (d1 * d1);
+            }
+            if (d2 != 0.0) {
+                b = (U[i + k + 1] - u) / d2;
+                if (kk == i + 1) db += (U[i + k + 1] - u) / (d2 * d2);
+                if (kk == i + k + 1) db += (u - U[i + 1]) / (d2 * d2);
+            }
+            double Nn = a * N[i] + b * N[i + 1];                                   /* Eq.4 */
+            double Dn = da * N[i] + a * D[i] + db * N[i + 1] + b * D[i + 1];       /* d/dU_kk */
+            N[i] = Nn;
+            D[i] = Dn;
+        }
+    }
+    for (int i = 0; i < n; ++i) dN_out[i] = D[i];
+    free(N);
+    free(D);
+}
+
+/* dL/dU, dL/dV for surfaces: dL/dU_kk = sum over points of g . dS/dU_kk with the quotient */
+/* rule of Eq.7's form: dS/dU_kk = (dNR W - NR dW) / W^2, where               */
+/* NR = sum_ij N_i N_j w_ij P_ij, W = sum_ij N_i N_j w_ij and dNR, dW replace N_i by        */
+/* dN_i/dU_kk (all i, j: the literal double sum). Shared knots (knots_batched = 0) give    */
+/* one gradient summed over the B surfaces; batched knots one per surface.                */
+/* gU [(kb ? B : 1)][n+p+1], gV [(kb ? B : 1)][m+q+1].                                     */
+int nurbs_ref_surface_knot_grad(int B, int n, int m, int p, int q, int n_u, int n_v, int knots_batched,
+                                const double* ctrl, const double* U, const double* V,
+                                const double* u, const double* v, const double* gout,
+                                double* gU, double* gV)
+{
+    if (p > REF_MAX_DEG || q > REF_MAX_DEG) return REF_E_ARG;
+    int st = check_common(B, n, m, p, q, n_u, n_v, knots_batched, ctrl, U, V, u, v);
+    if (st) return st;
+    const int nkU = n + p + 1, nkV = m + q + 1;
+    memset(gU, 0, sizeof(double) * (size_t)(knots_batched ? B : 1) * nkU);
+    memset(gV, 0, sizeof(double) * (size_t)(knots_batched ? B : 1) * nkV);
+    double* Nu = (double*)malloc(sizeof(double) * (size_t)n_u * n);
+    double* Nv = (double*)malloc(sizeof(double) * (size_t)n_v * m);
+    double* dNu = (double*)malloc(sizeof(double) * (size_t)n_u * n * nkU);
+    double* dNv = (double*)malloc(sizeof(double) * (size_t)n_v * m * nkV);
+    for (int k = 0; k < B; ++k) {
+        const double* Uk = U + (knots_batched ? (size_t)k * nkU : 0);
+        const double* Vk = V + (knots_batched ? (size_t)k * nkV : 0);
+        const double* Pk = ctrl + (size_t)k * n * m * 4;
+        double* gUk = gU + (knots_batched ? (size_t)k * nkU : 0);
+        double* gVk = gV + (knots_batched ? (size_t)k * nkV : 0);
+        if (k == 0 || knots_batched) {
+            for (int a = 0; a < n_u; ++a) {
+                nurbs_ref_basis_dense(n, p, Uk, u[a], Nu + (size_t)a * n);
+                for (int kk = 0; kk < nkU; ++kk)
+                    nurbs_ref_basis_dknot(n, p, Uk, u[a], kk, dNu + ((size_t)a * nkU + kk) * n);
+            }
+            for (int b = 0; b < n_v; ++b) {
+                nurbs_ref_basis_dense(m, q, Vk, v[b], Nv + (size_t)b * m);
+                for (int kk = 0; kk < nkV; ++kk)
+                    nurbs_ref_basis_dknot(m, q, Vk, v[b], kk, dNv + ((size_t)b * nkV + kk) * m);
+            }
+        }
+        for (int a = 0; a < n_u; ++a)
+            for (int b = 0; b < n_v; ++b) {
+                const double* g = gout + (((size_t)k * n_u + a) * n_v + b) * 3;
+                double NR[3] = {0, 0, 0}, W = 0;
+                for (int i = 0; i < n; ++i)
+                    for (int j = 0; j < m; ++j) {
+                        const double* P = Pk + ((size_t)i * m + j) * 4;
+                        double c = Nu[(size_t)a * n + i] * Nv[(size_t)b * m + j] * P[3];
+                        NR[0] += c * P[0]; NR[1] += c * P[1]; NR[2] += c * P[2]; W += c;
+                    }
+                for (int dir = 0; dir < 2; ++dir) {
+                    const int nk = dir == 0 ? nkU : nkV;
+                    for (int kk = 0; kk < nk; ++kk) {
+                        double dNR[3] = {0, 0, 0}, dW = 0;
+                        for (int i = 0; i < n; ++i)
+                            for (int j = 0; j < m; ++j) {
+                                const double* P = Pk + ((size_t)i * m + j) * 4;
+                                double c = dir == 0
+                                    ? dNu[((size_t)a * nkU + kk) * n + i] * Nv[(size_t)b * m + j] * P[3]
+                                    : Nu[(size_t)a * n + i] * dNv[((size_t)b * nkV + kk) * m + j] * P[3];
+                                dNR[0] += c * P[0]; dNR[1] += c * P[1]; dNR[2] += c * P[2]; dW += c;
+                            }
+                        double acc = 0.0;
+                        for (int cc = 0; cc < 3; ++cc) acc += g[cc] * (dNR[cc] * W - NR[cc] * dW) / (W * W);
+                        (dir == 0 ? gUk : gVk)[kk] += acc;
+                    }
+                }
+            }
+    }
+    free(Nu); free(Nv); free(dNu); free(dNv);
+    return REF_OK;
+}
+
+/* Curves: the same with the v-direction removed. gU [(kb ? B : 1)][n+p+1]. */
+int nurbs_ref_curve_knot_grad(int B, int n, int p, int n_u, int knots_batched, const double* ctrl,
+                              const double* U, const double* u, const double* gout, double* gU)
+{
+    if (p > REF_MAX_DEG || B < 0 || n_u < 0) return REF_E_ARG;
+    const int nk = n + p + 1;
+    memset(gU, 0, sizeof(double) * (size_t)(knots_batched ? B : 1) * nk);
+    double* N = (double*)malloc(sizeof(double) * (size_t)n);
+    double* dN = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int k = 0; k < B; ++k) {
+        const double* Uk = U + (knots_batched ? (size_t)k * nk : 0);
+        if (k == 0 || knots_batched) {
+            int st = nurbs_ref_check_knots(n, p, Uk);
+            if (st) { free(N); free(dN); return st; }
+        }
+        const double* Pk = ctrl + (size_t)k * n * 4;
+        double* gUk = gU + (knots_batched ? (size_t)k * nk : 0);
+        for (int a = 0; a < n_u; ++a) {
+            if (nurbs_ref_find_span(n, p, Uk, u[a]) < 0) { free(N); free(dN); return REF_E_DOMAIN; }
+            nurbs_ref_basis_dense(n, p, Uk, u[a], N);
+            const double* g = gout + ((size_t)k * n_u + a) * 3;
+            double NR[3] = {0, 0, 0}, W = 0;
+            for (int i = 0; i < n; ++i) {
+                const double* P = Pk + (size_t)i * 4;
+                double c = N[i] * P[3];
+                NR[0] += c * P[0]; NR[1] += c * P[1]; NR[2] += c * P[2]; W += c;
+            }
+            for (int kk = 0; kk < nk; ++kk) {
+                nurbs_ref_basis_dknot(n, p, Uk, u[a], kk, dN);
+                double dNR[3] = {0, 0, 0}, dW = 0;
+                for (int i = 0; i < n; ++i) {
+                    const double* P = Pk + (size_t)i * 4;
+                    double c = dN[i] * P[3];
+                    dNR[0] += c * P[0]; dNR[1] += c * P[1]; dNR[2] += c * P[2]; dW += c;
+                }
+                for (int cc = 0; cc < 3; ++cc) gUk[kk] += g[cc] * (dNR[cc] * W - NR[cc] * dW) / (W * W);
+            }
+        }
+    }
+    free(N); free(dN);
+    return REF_OK;
+}

@@ -593,3 +593,118 @@ def test_points_backward_invariants_and_errors():
     with pytest.raises(oracle.OracleError):
         oracle.surface_fwd_points(ctrl, U, V, bad, p, q)
     assert oracle.surface_fwd_points(ctrl, U, V, uv[:, :0], p, q).shape == (1, 0, 3)
+
+
+# ---------------------------------------------------------------- NEXT-4: knot gradients
+def distinct_knots(rng, n, p, lo=0.0, hi=1.0):
+    inner = np.sort(rng.uniform(0.1, 0.9, n - p - 1))
+    while n - p - 1 > 1 and np.min(np.diff(inner)) < 0.03:
+        inner = np.sort(rng.uniform(0.1, 0.9, n - p - 1))
+    return np.concatenate([[lo] * (p + 1), inner, [hi] * (p + 1)])
+
+
+def params_away_from(U, rng, k, margin=0.01):
+    out = []
+    while len(out) < k:
+        x = rng.uniform(0.02, 0.98)
+        if np.min(np.abs(np.asarray(U) - x)) > margin:
+            out.append(x)
+    return np.sort(np.array(out))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5])
+def test_basis_knot_derivative_fd(p):
+    rng = np.random.default_rng(300 + p)
+    n = p + 5
+    U = distinct_knots(rng, n, p)
+    h = 1e-7
+    for u in params_away_from(U, rng, 6):
+        for kk in range(n + p + 1):
+            fd, tol = fd_knot(lambda K_: oracle.basis_dense(n, p, K_, u), U, (kk,), h)
+            if fd is None:
+                continue
+            an = oracle.basis_dknot(n, p, U, u, kk)
+            assert np.max(np.abs(an - fd)) <= tol * max(1.0, np.max(np.abs(fd))), (kk, u)
+
+
+def fd_knot(f, K, idx, h):
+    """Central difference in knot K[idx] when both K +- h keep the vector non-decreasing,
+    else the one-sided difference that does (looser tolerance), else None."""
+    row = K[idx[:-1]] if K.ndim == 2 else K
+    k = idx[-1]
+    up_ok = k + 1 >= len(row) or row[k] + h <= row[k + 1]
+    dn_ok = k == 0 or row[k] - h >= row[k - 1]
+    Kp, Km = K.copy(), K.copy()
+    Kp[idx] += h
+    Km[idx] -= h
+    if up_ok and dn_ok:
+        return (f(Kp) - f(Km)) / (2 * h), 1e-6
+    if up_ok:
+        return (f(Kp) - f(K)) / h, 2e-5
+    if dn_ok:
+        return (f(K) - f(Km)) / h, 2e-5
+    return None, None
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_surface_knot_grad_fd_and_invariants(seed):
+    rng = np.random.default_rng(400 + seed)
+    B, p, q = 2, 1 + seed % 3, 1 + (seed + 1) % 3
+    n, m = p + 3 + seed % 2, q + 4
+    batched = bool(seed % 2)
+    if batched:
+        U = np.stack([distinct_knots(rng, n, p) for _ in range(B)])
+        V = np.stack([distinct_knots(rng, m, q) for _ in range(B)])
+        allU, allV = U.ravel(), V.ravel()
+    else:
+        U, V = distinct_knots(rng, n, p), distinct_knots(rng, m, q)
+        allU, allV = U, V
+    u = params_away_from(allU, rng, 7)
+    v = params_away_from(allV, rng, 5)
+    ctrl = np.empty((B, n, m, 4))
+    ctrl[..., :3] = rng.uniform(-1, 1, (B, n, m, 3))
+    ctrl[..., 3] = rng.uniform(0.5, 1.5, (B, n, m))
+    g = rng.normal(size=(B, len(u), len(v), 3))
+    gU, gV = oracle.surface_knot_grad(ctrl, U, V, u, v, g, p, q, batched)
+    h = 1e-7
+    L = lambda U_, V_: np.sum(oracle.surface_fwd(ctrl, U_, V_, u, v, p, q, batched) * g)
+    for which, K, G in (("U", U, gU), ("V", V, gV)):
+        for idx in np.ndindex(K.shape):
+            fd, tol = fd_knot(lambda K_: L(K_, V) if which == "U" else L(U, K_), K, idx, h)
+            if fd is None:
+                continue  # an inner copy of a clamped end knot: no order-preserving perturbation
+            gi = G[idx] if batched else G[0][idx]
+            assert abs(gi - fd) <= tol * max(1.0, np.max(np.abs(G))), (which, idx)
+    # translating all knots of a direction by d moves the parameters by -d (shift invariance):
+    # sum_k dL/dU_k = -sum g . S_u;  scaling knots and parameters together: sum_k U_k dL/dU_k = -sum u g . S_u
+    _, Su, Sv = oracle.surface_derivs(ctrl, U, V, u, v, p, q, batched)
+    gs = np.sum(g * Su, axis=(2, 3))            # [B][n_u]
+    gsv = np.sum(g * Sv, axis=(1, 3))           # [B][n_v]
+    sc = np.sum(np.abs(g)) * 10
+    if batched:
+        np.testing.assert_allclose(gU.sum(axis=1), -gs.sum(axis=1), atol=1e-12 * sc)
+        np.testing.assert_allclose((gU * U).sum(axis=1), -(gs * u).sum(axis=1), atol=1e-12 * sc)
+        np.testing.assert_allclose(gV.sum(axis=1), -gsv.sum(axis=1), atol=1e-12 * sc)
+    else:
+        assert abs(gU.sum() + gs.sum()) <= 1e-12 * sc
+        assert abs((gU[0] * U).sum() + (gs * u).sum()) <= 1e-12 * sc
+        assert abs(gV.sum() + gsv.sum()) <= 1e-12 * sc
+        assert abs((gV[0] * V).sum() + (gsv * v).sum()) <= 1e-12 * sc
+
+
+def test_curve_knot_grad_fd():
+    rng = np.random.default_rng(500)
+    for p in (1, 2, 3, 4):
+        n = p + 4
+        U = distinct_knots(rng, n, p)
+        u = params_away_from(U, rng, 9)
+        ctrl = np.empty((2, n, 4))
+        ctrl[..., :3] = rng.uniform(-1, 1, (2, n, 3))
+        ctrl[..., 3] = rng.uniform(0.5, 1.5, (2, n))
+        g = rng.normal(size=(2, len(u), 3))
+        gU = oracle.curve_knot_grad(ctrl, U, u, g, p)[0]
+        h = 1e-7
+        for kk in range(n + p + 1):
+            fd, tol = fd_knot(lambda K_: np.sum(oracle.curve_fwd(ctrl, K_, u, p) * g), U, (kk,), h)
+            if fd is not None:
+                assert abs(gU[kk] - fd) <= tol * max(1.0, np.max(np.abs(gU)))
