@@ -143,6 +143,30 @@ int    nurbs_surface_fit_step(const nurbs_shape* shape, float* ctrl,
 size_t nurbs_surface_fit_workspace_bytes(const nurbs_shape* shape);
 
 /* ---------------------------------------------------------------------------------------
+ * True knot gradients (NEXT-4). The paper defines dL/dU = dL/dV = 0 (§3.2.2), which is
+ * what nurbs_surface_bwd / nurbs_curve_bwd return. These calls return the same grad_ctrl and,
+ * in grad_U / grad_V (nullable: that direction is skipped), the derivative of L with respect
+ * to every knot: the A2.2 basis differentiated along the 2p knots it reads, at each
+ * sample's span (spans held fixed: the derivative exists where no sample sits on a knot):
+ *     dL/dU_k = sum_points g . dS/dU_k,   dS/dU_k = (dNR W - NR dW) / W^2   (Eq.7's form).
+ * Shared knots (knots_batched = 0) give ONE gradient summed over the B surfaces; batched knots
+ * one per surface. u / v must be non-decreasing (the grid); U, V, u, v may not be NULL even
+ * with tables. Workspace: nurbs_*_bwd_knots_workspace_bytes(shape) bytes (never 0).
+ * Deterministic (fixed-order sums). Curves: grad_U receives the curve's knot gradient.
+ * --------------------------------------------------------------------------------------- */
+int    nurbs_surface_bwd_knots(const nurbs_shape* shape, const float* ctrl,
+                               const float* U, const float* V, const float* u, const float* v,
+                               const void* tables, const float* grad_out,
+                               float* grad_ctrl, float* grad_U, float* grad_V,
+                               void* workspace, size_t ws_bytes, void* stream);
+size_t nurbs_surface_bwd_knots_workspace_bytes(const nurbs_shape* shape);
+int    nurbs_curve_bwd_knots(const nurbs_shape* shape, const float* ctrl, const float* U,
+                             const float* u, const void* tables, const float* grad_out,
+                             float* grad_ctrl, float* grad_U,
+                             void* workspace, size_t ws_bytes, void* stream);
+size_t nurbs_curve_bwd_knots_workspace_bytes(const nurbs_shape* shape);
+
+/* ---------------------------------------------------------------------------------------
  * Paired (scattered) parameter points (NEXT-1): point t of surface k is evaluated at its own
  * (u, v) = uv[k][t] — S(u, v) anywhere in the domain with the per-point span and
  * basis of Alg.1, the same Eq.3 sum and Eq.8/9 gradient as the grid calls.

@@ -33,4 +33,9 @@ from .api import (  # noqa: F401
     nurbs_validate_points,
     surface_points_fwd,
     surface_points_bwd,
+    knots_workspace_bytes,
+    nurbs_surface_bwd_knots,
+    nurbs_curve_bwd_knots,
+    surface_bwd_knots,
+    curve_bwd_knots,
 )

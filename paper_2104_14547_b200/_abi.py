@@ -24,7 +24,9 @@ EXPORTS = ["nurbs_tables_bytes", "nurbs_tables", "nurbs_surface_fwd", "nurbs_sur
            "nurbs_curve_bwd_workspace_bytes", "nurbs_validate", "nurbs_strerror",
            "nurbs_surface_fit_step", "nurbs_surface_fit_workspace_bytes", "nurbs_surface_derivs",
            "nurbs_last_error_detail", "nurbs_abi_version", "nurbs_surface_points_fwd",
-           "nurbs_surface_points_bwd", "nurbs_surface_points_bwd_workspace_bytes", "nurbs_validate_points"]
+           "nurbs_surface_points_bwd", "nurbs_surface_points_bwd_workspace_bytes", "nurbs_validate_points",
+           "nurbs_surface_bwd_knots", "nurbs_surface_bwd_knots_workspace_bytes", "nurbs_curve_bwd_knots",
+           "nurbs_curve_bwd_knots_workspace_bytes"]
 
 
 class nurbs_shape(ctypes.Structure):
@@ -69,6 +71,10 @@ def load() -> ctypes.CDLL:
         "nurbs_surface_points_bwd": ([sh, P, P, P, P, P, P, P, P, P, S, P], I),
         "nurbs_surface_points_bwd_workspace_bytes": ([sh], S),
         "nurbs_validate_points": ([sh, P, P, P, P, P], I),
+        "nurbs_surface_bwd_knots": ([sh, P, P, P, P, P, P, P, P, P, P, P, S, P], I),
+        "nurbs_surface_bwd_knots_workspace_bytes": ([sh], S),
+        "nurbs_curve_bwd_knots": ([sh, P, P, P, P, P, P, P, P, S, P], I),
+        "nurbs_curve_bwd_knots_workspace_bytes": ([sh], S),
         "nurbs_strerror": ([I], ctypes.c_char_p),
         "nurbs_last_error_detail": ([], ctypes.c_char_p),
         "nurbs_abi_version": ([], I),

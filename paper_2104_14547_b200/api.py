@@ -131,6 +131,49 @@ def nurbs_validate(sh, ctrl, U, V, u, v, stream=None):
                                 _stream(stream)), "nurbs_validate")
 
 
+# ----------------------------------------------------------------------------- knot gradients (NEXT-4)
+def knots_workspace_bytes(sh: nurbs_shape) -> int:
+    L = load()
+    f = L.nurbs_curve_bwd_knots_workspace_bytes if _is_curve(sh) else L.nurbs_surface_bwd_knots_workspace_bytes
+    return int(f(ctypes.byref(sh)))
+
+
+def nurbs_surface_bwd_knots(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes,
+                            stream=None):
+    check(load().nurbs_surface_bwd_knots(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
+                                         _ptr(tables), _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U), _ptr(grad_V),
+                                         _ptr(workspace), ctypes.c_size_t(ws_bytes), _stream(stream)),
+          "nurbs_surface_bwd_knots")
+
+
+def nurbs_curve_bwd_knots(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspace, ws_bytes, stream=None):
+    check(load().nurbs_curve_bwd_knots(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(u), _ptr(tables), _ptr(grad_out),
+                                       _ptr(grad_ctrl), _ptr(grad_U), _ptr(workspace), ctypes.c_size_t(ws_bytes),
+                                       _stream(stream)), "nurbs_curve_bwd_knots")
+
+
+def surface_bwd_knots(ctrl, U, V, u, v, grad_out, p: int, q: int, tables=None, stream=None):
+    """(grad_ctrl, dL/dU, dL/dV) with TRUE knot gradients (NEXT-4); dL/dU is [n+p+1] for
+    shared knots (summed over the batch) or [B][n+p+1] for batched knots."""
+    sh = surface_shape(ctrl, U, u, v, p, q)
+    grad_ctrl = torch.empty_like(ctrl)
+    gU, gV = torch.empty_like(U), torch.empty_like(V)
+    ws = knots_workspace_bytes(sh)
+    work = torch.empty(max(ws, 1), dtype=torch.uint8, device=ctrl.device)
+    nurbs_surface_bwd_knots(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, gU, gV, work, ws, stream)
+    return grad_ctrl, gU, gV
+
+
+def curve_bwd_knots(ctrl, U, u, grad_out, p: int, tables=None, stream=None):
+    sh = curve_shape(ctrl, U, u, p)
+    grad_ctrl = torch.empty_like(ctrl)
+    gU = torch.empty_like(U)
+    ws = knots_workspace_bytes(sh)
+    work = torch.empty(max(ws, 1), dtype=torch.uint8, device=ctrl.device)
+    nurbs_curve_bwd_knots(sh, ctrl, U, u, tables, grad_out, grad_ctrl, gU, work, ws, stream)
+    return grad_ctrl, gU
+
+
 # ----------------------------------------------------------------------------- paired points (NEXT-1)
 def points_shape(ctrl: torch.Tensor, U: torch.Tensor, uv: torch.Tensor, p: int, q: int) -> nurbs_shape:
     B, n, m, four = ctrl.shape

@@ -28,7 +28,8 @@ def units():
     u = [("nurbs_api", os.path.join(CSRC, "nurbs_api.cu"), []),
          ("nurbs_kernels", os.path.join(CSRC, "nurbs_kernels.cu"), []),
          ("nurbs_derivs", os.path.join(CSRC, "nurbs_derivs.cu"), []),
-         ("nurbs_points", os.path.join(CSRC, "nurbs_points.cu"), [])]
+         ("nurbs_points", os.path.join(CSRC, "nurbs_points.cu"), []),
+         ("nurbs_knots", os.path.join(CSRC, "nurbs_knots.cu"), [])]
     for p in range(6):
         u.append((f"nurbs_grid_p{p}", os.path.join(CSRC, "nurbs_grid_p.cu"), [f"-DNB_P={p}"]))
     for p in range(1, 6):

@@ -13,6 +13,7 @@
 #include "nurbs_internal.cuh"
 #include "nurbs_points.cuh"
 #include "nurbs_points_plan.h"
+#include "nurbs_knots.h"
 
 using nb::Dir;
 using nb::Params;
@@ -245,6 +246,84 @@ int check_ptrs(bool bwd, const void* ctrl, const void* out, const void* gout, co
   return NURBS_OK;
 }
 
+// ---- true knot gradients (NEXT-4): workspace = the backward's + partials + assembly buffers
+struct KnotWs {
+  size_t hU, hV, cR, sR, cC, sC, tR, tC, bytes;
+};
+KnotWs knot_ws(const Geo& g, const Plan& pl) {
+  KnotWs w{};
+  const size_t B = (size_t)g.B;
+  size_t o = nb::align_up(pl.ws_bytes, 256);
+  auto take = [&](size_t bytes) { const size_t at = o; o = nb::align_up(o + bytes, 256); return at; };
+  w.hU = take(B * pl.NCB * g.r.ns * (g.P + 1) * 4);
+  w.hV = take(B * pl.NRB * g.c.ns * (g.c.p + 1) * 4);
+  w.cR = take(B * g.r.ns * 2 * g.P * 4);
+  w.sR = take(B * g.r.ns * 4);
+  w.cC = take(B * g.c.ns * 2 * g.c.p * 4);
+  w.sC = take(B * g.c.ns * 4);
+  w.tR = take(B * (g.r.n + g.P + 1) * 4);
+  w.tC = take(B * (g.c.n + g.c.p + 1) * 4);
+  w.bytes = o;
+  return w;
+}
+
+int launch_knots(const Geo& g, const float* ctrl, const float* gout, float* gctrl, float* gR, float* gC, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns);
+  if (g.B == 0) return NURBS_OK;
+  const int gR_n = (g.r.n + g.r.p + 1) * (g.r.kstride ? g.B : 1);
+  const int gC_n = (g.c.n + g.c.p + 1) * (g.c.kstride ? g.B : 1);
+  if (g.r.ns == 0 || g.c.ns == 0) {  // no points: every gradient is zero
+    cudaError_t e = cudaMemsetAsync(gctrl, 0, (size_t)g.B * g.r.n * g.c.n * 16, st);
+    if (e == cudaSuccess && gR) e = cudaMemsetAsync(gR, 0, sizeof(float) * gR_n, st);
+    if (e == cudaSuccess && gC) e = cudaMemsetAsync(gC, 0, sizeof(float) * gC_n, st);
+    return e == cudaSuccess ? NURBS_OK : cuda_fail(e, "zero-fill");
+  }
+  if (pl.grid > 0x7fffffffLL) return fail(NURBS_E_ARG, "grid of %lld CTAs too large", pl.grid);
+  const KnotWs W = knot_ws(g, pl);
+  if (!ws || ws_bytes < W.bytes)
+    return fail(NURBS_E_WORKSPACE, "backward with knot gradients needs a %zu-byte workspace (got %zu at %p)", W.bytes,
+                ws_bytes, ws);
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  Params prm{};
+  prm.B = g.B;
+  prm.r = g.r;
+  prm.c = g.c;
+  prm.ctrl = reinterpret_cast<const float4*>(ctrl);
+  prm.gout = gout;
+  prm.gctrl = reinterpret_cast<float4*>(gctrl);
+  prm.K = pl.K;
+  prm.NRB = pl.NRB;
+  prm.NCB = pl.NCB;
+  prm.T_rows = pl.T_rows;
+  prm.CBW = g.c.n < nb::kBandCols ? g.c.n : nb::kBandCols;
+  prm.direct = pl.direct;
+  prm.bulk = (g.c.ns % 4 == 0) && aligned16(gout) ? 1 : 0;
+  if (getenv("NURBS_NO_TMA")) prm.bulk = 0;
+  if (!pl.direct) {
+    prm.slots = reinterpret_cast<float4*>(w);
+    prm.colband = reinterpret_cast<int2*>(w + pl.slots_bytes);
+  }
+  prm.hU = reinterpret_cast<float*>(w + W.hU);
+  prm.hV = reinterpret_cast<float*>(w + W.hV);
+  cudaError_t e = nb::launch_grid(prm, 3, g.P, g.c.p, st);
+  if (e != cudaSuccess) return cuda_fail(e, "backward (knot gradients) kernel launch");
+  if (!pl.direct && (e = nb::launch_reduce(prm, g.P, st)) != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
+  if (g.P > 0 && gR) {
+    nb::KnotDir d{g.B, g.r.n, g.P, g.r.ns, g.r.knots, g.r.kstride, g.r.s, g.r.tspan, prm.hU, pl.NCB,
+                  reinterpret_cast<float*>(w + W.cR), reinterpret_cast<int*>(w + W.sR)};
+    e = nb::launch_knot_grad(d, g.r.kstride != 0, reinterpret_cast<float*>(w + W.tR), gR, st);
+    if (e != cudaSuccess) return cuda_fail(e, "knot-gradient kernels (u)");
+  }
+  if (gC) {
+    nb::KnotDir d{g.B, g.c.n, g.c.p, g.c.ns, g.c.knots, g.c.kstride, g.c.s, g.c.tspan, prm.hV, pl.NRB,
+                  reinterpret_cast<float*>(w + W.cC), reinterpret_cast<int*>(w + W.sC)};
+    e = nb::launch_knot_grad(d, g.c.kstride != 0, reinterpret_cast<float*>(w + W.tC), gC, st);
+    if (e != cudaSuccess) return cuda_fail(e, "knot-gradient kernels (v)");
+  }
+  return NURBS_OK;
+}
+
 // ---- paired points (NEXT-1)
 int check_points_shape(const nurbs_shape* sh) {
   if (!sh) return fail(NURBS_E_ARG, "shape is NULL");
@@ -304,6 +383,54 @@ int points_common(const nurbs_shape* sh, const float* ctrl, const float* U, cons
 }  // namespace
 
 extern "C" {
+
+size_t nurbs_surface_bwd_knots_workspace_bytes(const nurbs_shape* sh) {
+  if (!sh || sh->B <= 0 || sh->n <= sh->p || sh->m <= sh->q || sh->n_u < 0 || sh->n_v < 0) return 0;
+  Geo g = surface_geo(sh, nullptr, nullptr, nullptr, nullptr);
+  return knot_ws(g, nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns)).bytes;
+}
+
+size_t nurbs_curve_bwd_knots_workspace_bytes(const nurbs_shape* sh) {
+  if (!sh || sh->B <= 0 || sh->n <= sh->p || sh->n_u < 0) return 0;
+  Geo g = curve_geo(sh, nullptr, nullptr);
+  return knot_ws(g, nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns)).bytes;
+}
+
+int nurbs_surface_bwd_knots(const nurbs_shape* sh, const float* ctrl, const float* U, const float* V, const float* u,
+                            const float* v, const void* tables, const float* grad_out, float* grad_ctrl, float* grad_U,
+                            float* grad_V, void* workspace, size_t ws_bytes, void* stream) {
+  g_detail.clear();
+  int st = check_surface_shape(sh);
+  if (st) return st;
+  if (sh->B == 0) return NURBS_OK;
+  if (!grad_ctrl) return fail(NURBS_E_ARG, "grad_ctrl is NULL");
+  if (!U || !V || !u || !v) return fail(NURBS_E_ARG, "knot gradients need U, V, u and v");
+  if (sh->n_u > 0 && sh->n_v > 0 && (st = check_ptrs(true, ctrl, nullptr, grad_out, grad_ctrl))) return st;
+  if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = surface_geo(sh, U, V, u, v);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  attach_tables(g, tables);
+  return launch_knots(g, ctrl, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes, s);
+}
+
+int nurbs_curve_bwd_knots(const nurbs_shape* sh, const float* ctrl, const float* U, const float* u, const void* tables,
+                          const float* grad_out, float* grad_ctrl, float* grad_U, void* workspace, size_t ws_bytes,
+                          void* stream) {
+  g_detail.clear();
+  int st = check_curve_shape(sh);
+  if (st) return st;
+  if (sh->B == 0) return NURBS_OK;
+  if (!grad_ctrl) return fail(NURBS_E_ARG, "grad_ctrl is NULL");
+  if (!U || !u) return fail(NURBS_E_ARG, "knot gradients need U and u");
+  if (sh->n_u > 0 && (st = check_ptrs(true, ctrl, nullptr, grad_out, grad_ctrl))) return st;
+  if (tables && sh->knots_batched) return fail(NURBS_E_TABLES, "tables need shared knots (knots_batched = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geo g = curve_geo(sh, U, u);
+  if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
+  attach_tables(g, tables);
+  return launch_knots(g, ctrl, grad_out, grad_ctrl, nullptr, grad_U, workspace, ws_bytes, s);
+}
 
 size_t nurbs_surface_points_bwd_workspace_bytes(const nurbs_shape* sh) {
   if (!sh || sh->B <= 0 || sh->n_u <= 0 || sh->n <= sh->p || sh->m <= sh->q || sh->p < 1 || sh->q < 1) return 0;

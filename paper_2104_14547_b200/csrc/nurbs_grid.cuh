@@ -31,10 +31,10 @@ namespace nb {
 // One row of the walk (F2, and B1 in the backward) for one column: uniform across the CTA
 // except for the column data. `nu` = basis of the row, `tw` = the T window (P+1 control rows
 // [lo, lo+P] of this column), `io` = this thread's 3 floats of the output / dL/dS row.
-template <int P, bool BWD, bool FIT>
+template <int P, bool BWD, bool FIT, bool KG>
 __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const float4 (&tw)[P + 1],
                                          float4 (&acc)[P + 1], float* io, bool valid, float fit_scale,
-                                         float& lsum) {
+                                         float& lsum, float (&dots)[P + 1]) {
   float4 Sp = f4(0.f);
 #pragma unroll
   for (int k = 0; k <= P; ++k) Sp = fma4v(nu[k], tw[k], Sp);
@@ -72,6 +72,10 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
     const float4 G = make_float4(gxy.x, gxy.y, gzr, -gS * rw);
 #pragma unroll
     for (int k = 0; k <= P; ++k) acc[k] = fma4v(nu[k], G, acc[k]);
+    if constexpr (KG) {  // NEXT-4: G . T_r, the row's weight of dN_r/dU
+#pragma unroll
+      for (int k = 0; k <= P; ++k) dots[k] = fmaf(G.x, tw[k].x, fmaf(G.y, tw[k].y, fmaf(G.z, tw[k].z, G.w * tw[k].w)));
+    }
   }
 }
 
@@ -192,9 +196,10 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
   __syncthreads();  // ring slots free again
 }
 
-template <int P, int Q, bool BWD, bool BULK, bool FIT>
+template <int P, int Q, bool BWD, bool BULK, bool FIT, bool KG>
 __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) nurbs_grid_kernel(const Params prm) {
   static_assert(!FIT || BWD, "the fitting step is a backward variant");
+  static_assert(!KG || (BWD && !FIT), "knot gradients extend the plain backward");
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   uint64_t* sfull = bars + 1;           // bwd: stage slot filled by TMA (count 1 + tx bytes)
   uint64_t* sempty = bars + 1 + NST;    // fwd: stage slot drained by TMA (count 1)
   int* scnt = reinterpret_cast<int*>(bars + 1 + 2 * NST);  // per slot: warps done with the stage
+  float* rowdot = reinterpret_cast<float*>(scnt + NST + 2);  // KG: [4 warps][kRowChunk][P+1]
 
   if (tid == 0) {
     mbar_init(band_bar, 1u);
@@ -417,7 +423,20 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   int b2_next = band_lo;  // first completed control row not yet reduced by B2
   // row i complete (uniform across the CTA): H(i) -> ring. The fast variant never reduces
   // (the stage loop guarantees ring capacity); the checked one reduces a full ring.
-  auto flush_fast = [&](int i, float4 h) { Hring[((i - band_lo) & (kHRing - 1)) * kCB + tid] = h; };
+  float hv[Q + 1];  // KG: this column's sum over control rows i of Q[i][sv-q+h] . H[i][b]
+#pragma unroll
+  for (int h = 0; h <= Q; ++h) hv[h] = 0.f;
+  auto flush_fast = [&](int i, float4 hrow) {
+    Hring[((i - band_lo) & (kHRing - 1)) * kCB + tid] = hrow;
+    if constexpr (KG) {
+      const float4* src = tb0 + (size_t)i * tstride;
+#pragma unroll
+      for (int h = 0; h <= Q; ++h) {
+        const float4 q4 = homog(src[h]);
+        hv[h] = fmaf(q4.x, hrow.x, fmaf(q4.y, hrow.y, fmaf(q4.z, hrow.z, fmaf(q4.w, hrow.w, hv[h]))));
+      }
+    }
+  };
   auto flush_checked = [&](int i, float4 h) {
     flush_fast(i, h);
     if (i + 1 - b2_next == kHRing) {
@@ -437,7 +456,35 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   }
 
   // TMA staging: columns >= cols use the unused row tail (the fit step still masks its loss)
-  const bool vio = (BULK && !FIT) ? true : valid;
+  const bool vio = (BULK && !FIT && !KG) ? true : valid;
+  // KG: the warp sums of G . T_r for one walk row -> rowdot[warp][ci][r]
+  auto kg_row = [&](int ci, const float (&d)[P + 1]) {
+    if constexpr (KG) {
+      float x[P + 1];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) x[k] = d[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int k = 0; k <= P; ++k) x[k] += __shfl_xor_sync(0xffffffffu, x[k], o);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k <= P; ++k) rowdot[(warp * kRowChunk + ci) * (P + 1) + k] = x[k];
+    }
+  };
+  // KG: rows [r0, r0 + cn) of the walk are complete in rowdot (after a barrier): warp sums in
+  // warp order -> hU[s][cb][a][r] (fixed-order partial of the column block)
+  auto kg_flush = [&](int r0, int cn) {
+    if constexpr (KG) {
+      for (int x = tid; x < cn * (P + 1); x += kThreads) {
+        const int row = x / (P + 1), k = x - row * (P + 1);
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) v += rowdot[(w * kRowChunk + row) * (P + 1) + k];
+        prm.hU[(((size_t)s * prm.NCB + cb) * R.ns + a_lo + r0 + row) * (P + 1) + k] = v;
+      }
+    }
+  };
   const float fit_scale = prm.fit_scale;
   float lsum = 0.f;  // FIT: this thread's sum of |S - T|^2
   // One row of the walk: advance the window to the row's span if it changed (uniform across
@@ -465,7 +512,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
       const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
       nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
     }
-    walk_row<P, BWD, FIT>(nu, tw, acc, io, vio, fit_scale, lsum);
+    float dots[P + 1];
+    walk_row<P, BWD, FIT, KG>(nu, tw, acc, io, vio, fit_scale, lsum, dots);
+    kg_row(ci, dots);
   };
   // rows [r0, r0+nr) of the walk: unrolled fast paths when the window does not move (no span
   // checks at all) or when the H ring cannot overflow
@@ -482,7 +531,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
           const float4 n1 = *reinterpret_cast<const float4*>(nup + 4);
           nu[4] = n1.x; nu[5] = n1.y; nu[6] = n1.z; nu[7] = n1.w;
         }
-        walk_row<P, BWD, FIT>(nu, tw, acc, io0 + r * io_stride, vio, fit_scale, lsum);
+        float dots[P + 1];
+        walk_row<P, BWD, FIT, KG>(nu, tw, acc, io0 + r * io_stride, vio, fit_scale, lsum, dots);
+        kg_row(ci0 + r, dots);
       }
       return;
     }
@@ -515,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     const int ci0 = r0 % kRowChunk;           // kRowChunk is a multiple of RPS
     if (ci0 == 0) {                           // stage span + basis of the next kRowChunk rows
       if (r0 > 0) __syncthreads();            // previous chunk fully consumed
+      if (KG && r0 > 0) kg_flush(r0 - kRowChunk, kRowChunk);
       const int cn = min(kRowChunk, nwalk - r0);
       if (tid < cn) {
         const int a = a_lo + r0 + tid;
@@ -567,6 +619,10 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     if (++slot == NST) { slot = 0; ++use; }
   }
   if constexpr (BULK && !BWD) bulk_wait_all();  // every store this thread issued has landed
+  if constexpr (KG) {
+    __syncthreads();
+    if (nwalk > 0) kg_flush((nstage - 1) * RPS / kRowChunk * kRowChunk, nwalk - (nstage - 1) * RPS / kRowChunk * kRowChunk);
+  }
 
   if constexpr (BWD) {
     // ---- B1 epilogue: flush the last window and the rows never reached (zeros), in order
@@ -584,8 +640,13 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
       __syncthreads();
       if (tid == 0) prm.loss_parts[blockIdx.x] = (lw[0] + lw[1]) + (lw[2] + lw[3]);
     }
+    if constexpr (KG) {  // this tile's partial of hV[s][rb][b][h]
+      if (valid)
+#pragma unroll
+        for (int h = 0; h <= Q; ++h) prm.hV[(((size_t)s * prm.NRB + rb) * C.ns + B0 + tid) * (Q + 1) + h] = hv[h];
+    }
     if (!prm.direct && rb == 0 && tid == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sfirst - Q, sfirst + nspan - 1);
-    if (prm.direct) {  // knot gradients are zero by definition
+    if (prm.direct && !KG) {  // knot gradients are zero by definition
       if (prm.gR && s < prm.gR_items)
         for (int x = tid; x < prm.gR_per; x += kThreads) prm.gR[(size_t)s * prm.gR_per + x] = 0.f;
       if (prm.gC && s < prm.gC_items)
@@ -594,24 +655,26 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   }
 }
 
-template <int P, int Q, bool BWD, bool BULK, bool FIT>
+template <int P, int Q, bool BWD, bool BULK, bool FIT, bool KG = false>
 static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
-  const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows, prm.CBW);
+  const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows, prm.CBW, KG);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, BULK, FIT>,
+    cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, BULK, FIT, KG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  nurbs_grid_kernel<P, Q, BWD, BULK, FIT>
+  nurbs_grid_kernel<P, Q, BWD, BULK, FIT, KG>
       <<<(unsigned)((long long)prm.B * prm.NRB * prm.NCB), kThreads, smem, st>>>(prm);
   return cudaGetLastError();
 }
 
-// mode: 0 forward, 1 backward, 2 fused fitting step (backward with dL/dS from a target)
+// mode: 0 forward, 1 backward, 2 fused fitting step (backward with dL/dS from a target),
+// 3 backward with the knot-gradient partials (NEXT-4)
 template <int P, int Q>
 static cudaError_t launch_pq(const Params& prm, int mode, cudaStream_t st) {
+  if (mode == 3) return prm.bulk ? launch_one<P, Q, true, true, false, true>(prm, st) : launch_one<P, Q, true, false, false, true>(prm, st);
   if (mode == 2) return prm.bulk ? launch_one<P, Q, true, true, true>(prm, st) : launch_one<P, Q, true, false, true>(prm, st);
   if (mode == 1) return prm.bulk ? launch_one<P, Q, true, true, false>(prm, st) : launch_one<P, Q, true, false, false>(prm, st);
   return prm.bulk ? launch_one<P, Q, false, true, false>(prm, st) : launch_one<P, Q, false, false, false>(prm, st);

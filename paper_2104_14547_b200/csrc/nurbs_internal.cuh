@@ -98,6 +98,9 @@ struct Params {
   float4* ctrl_mut;         // ctrl updated in place: P -= lr dL/dP, w -= lr dL/dw (Eq.14)
   float lr;
   int n_parts;
+  // true knot gradients (NEXT-4, mode 3)
+  float* hU;                // [B][NCB][r.ns][P+1]: sum over the block's columns of G . T_r
+  float* hV;                // [B][NRB][c.ns][q+1]: sum over the band rows of Q[i][sv-q+h] . H[i][b]
 };
 
 // Tables blob layout (nurbs_tables): header then four arrays, each 256-byte aligned.
@@ -171,7 +174,7 @@ cudaError_t launch_tables(const Dir& r, const Dir& c, void* tables, const TabLay
 cudaError_t launch_validate(int B, const Dir& r, const Dir& c, int check_rows,
                             const float4* ctrl, long long n_ctrl,
                             unsigned long long* status, cudaStream_t st);
-size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW);
+size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg = false);
 
 }  // namespace nb
 

@@ -140,7 +140,7 @@ __global__ void nurbs_validate_kernel(int B, Dir R, Dir C, int check_rows, const
 }
 
 // ------------------------------------------------------------------------ launchers
-size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW) {
+size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg) {
   const int NP = (P + 1) <= 4 ? 4 : 8;
   const int NQ = (q + 1) <= 4 ? 4 : 8;
   const int rps = bwd ? kRPS_B : kRPS_F, nst = bwd ? kStages_B : kStages_F;
@@ -149,6 +149,7 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW) {
   if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4 + (kCB + 4) * 4;
   b += 4 * 4;                                  // misc
   b = (b + 7) / 8 * 8 + (1 + 2 * nst) * 8 + nst * 4;  // mbarriers + stage counters
+  if (kg) b += 8 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4;  // rowdot (NEXT-4)
   return b;
 }
 

@@ -1,0 +1,25 @@
+// nurbs_knots.h — host-visible pieces of the knot-gradient assembly (NEXT-4, nurbs_knots.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+
+#define NURBS_MAXD 5
+
+namespace nb {
+
+struct KnotDir {             // one parametric direction
+  int B, n, p, ns;           // surfaces, control count, degree, samples
+  const float* knots;        // [n+p+1] or batched
+  long long kstride;         // 0 = shared
+  const float* samples;      // [ns], non-decreasing
+  const int* tspan;          // optional span table
+  const float* part;         // [B][nparts][ns][p+1] partial h
+  int nparts;
+  float* contrib;            // [B][ns][2p] workspace
+  int* span;                 // [B][ns] workspace
+};
+
+// dL/d(knots) of one direction into out ([B][nk] if batched, else [nk] via tmp [B][nk]).
+cudaError_t launch_knot_grad(const KnotDir& d, bool batched, float* tmp, float* out, cudaStream_t st);
+
+}  // namespace nb

@@ -1,0 +1,114 @@
+"""GPU parity of the true knot gradients (NEXT-4) against the fp64 oracle
+(oracle.surface_knot_grad / curve_knot_grad, pinned by finite differences and the
+shift / scale invariants in test_oracle_pins.py), through the C ABI. Tolerance: normwise
+1e-4 per direction per surface (or for the batch sum with shared knots), like the other
+gradients (R16). The control-point gradient of the same call equals nurbs_surface_bwd's bitwise.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_14547_b200 as nb  # noqa: E402
+from test_gpu_parity import BWD_TOL, T  # noqa: E402
+
+KTOL = BWD_TOL
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2104_14547_b200.build import build
+    build()
+    oracle.build()
+
+
+def kerr(gpu, ref):
+    gpu, ref = np.atleast_2d(gpu), np.atleast_2d(ref)
+    sc = np.abs(ref).max(axis=1)
+    sc[sc == 0] = 1.0
+    return float(np.max(np.abs(gpu - ref).max(axis=1) / sc))
+
+
+def run(w, g, tables=False):
+    ctrl, U, V, u, v = T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v)
+    tab = nb.Tables.build(nb.surface_shape(ctrl, U, u, v, w.p, w.q), U, V, u, v) if tables else None
+    gc, gU, gV = nb.surface_bwd_knots(ctrl, U, V, u, v, T(g), w.p, w.q, tables=tab)
+    plain = nb.surface_bwd(ctrl, U, V, u, v, T(g), w.p, w.q, tables=tab)
+    torch.cuda.synchronize()
+    assert torch.equal(gc, plain), "control gradient must equal nurbs_surface_bwd's bitwise"
+    return gU.cpu().numpy(), gV.cpu().numpy()
+
+
+def check(w, g=None, tables=False):
+    g = w.grad_out() if g is None else g
+    gU, gV = run(w, g, tables)
+    rU, rV = oracle.surface_knot_grad(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q, w.knots_batched)
+    if not w.knots_batched:
+        rU, rV = rU[0], rV[0]
+    assert kerr(gU, rU) <= KTOL and kerr(gV, rV) <= KTOL, (kerr(gU, rU), kerr(gV, rV))
+
+
+@pytest.mark.parametrize("p,q", [(1, 1), (2, 3), (3, 3), (3, 1), (4, 2), (5, 5)])
+@pytest.mark.parametrize("batched", [False, True])
+def test_knot_grad_parity_degrees(p, q, batched):
+    rng = np.random.default_rng(50 + 10 * p + q + (7 if batched else 0))
+    n, m = int(rng.integers(p + 1, p + 8)), int(rng.integers(q + 1, q + 8))
+    w = wl.surfaces(f"k{p}{q}", 3, n, m, p, q, 37, 29, seed=p + 5 * q, knots_batched=batched)
+    check(w)
+
+
+def test_knot_grad_tiled_and_tables():
+    """Several row and column blocks (the reduce path, several partials per sample)."""
+    w = wl.surfaces("tiled", 1, 12, 10, 3, 3, 50, 260, seed=8)   # NRB = 9 row blocks, NCB = 3
+    check(w)
+    w2 = wl.config2()
+    check(w2, tables=True)
+
+
+def test_knot_grad_config1_curve():
+    c = wl.config1()
+    g = c.grad_out()
+    ctrl, U, u = T(c.ctrl), T(c.U), T(c.u)
+    gc, gU = nb.curve_bwd_knots(ctrl, U, u, T(g), c.p)
+    plain = nb.curve_bwd(ctrl, U, u, T(g), c.p)
+    torch.cuda.synchronize()
+    assert torch.equal(gc, plain)
+    ref = oracle.curve_knot_grad(c.ctrl, c.U, c.u, g, c.p)[0]
+    assert kerr(gU.cpu().numpy(), ref) <= KTOL
+
+
+def test_knot_grad_repeatable_and_shift_invariant_full_cfg4():
+    """Full config 4 (4096 surfaces, shared knots: one gradient summed over the batch): bitwise
+    repeatable, and sum_k dL/dU_k = -sum g . S_u with S_u from the (separately pinned) GPU
+    derivative kernel — a property that holds at any size."""
+    w = wl.config4()
+    g = w.grad_out()
+    a = run(w, g)
+    b = run(w, g)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    _, Su, Sv, _ = nb.surface_derivs(T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v), 3, 3, with_points=False,
+                                     with_normals=False)
+    gt = T(g).double()
+    su = float((gt * Su.double()).sum())
+    sv = float((gt * Sv.double()).sum())
+    scale = float(np.abs(a[0]).sum() + abs(su))
+    assert abs(float(a[0].astype(np.float64).sum()) + su) <= 1e-4 * scale
+    assert abs(float(a[1].astype(np.float64).sum()) + sv) <= 1e-4 * float(np.abs(a[1]).sum() + abs(sv))
+
+
+def test_knot_grad_full_cfg4_batched_sampled():
+    """Config 4 with per-surface knots at full size: sampled surfaces against the oracle."""
+    w = wl.config4(knots_batched=True)
+    g = w.grad_out()
+    gU, gV = run(w, g)
+    for k in (0, 4095):
+        sub = wl.Surfaces("s", 3, 3, w.ctrl[k:k + 1], w.U[k:k + 1], w.V[k:k + 1], w.u, w.v, True)
+        rU, rV = oracle.surface_knot_grad(sub.ctrl, sub.U, sub.V, sub.u, sub.v, g[k:k + 1], 3, 3, True)
+        assert kerr(gU[k:k + 1], rU) <= KTOL and kerr(gV[k:k + 1], rV) <= KTOL
