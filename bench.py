@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--derivs", action="store_true", help="time the NEXT-3 derivative kernel instead")
+    ap.add_argument("--knots", action="store_true",
+                    help="time the NEXT-4 backward with true knot gradients (nurbs_surface_bwd_knots) on the config")
     ap.add_argument("--paired", action="store_true",
                     help="time the NEXT-1 paired-points path on cfg4p (cfg4's nets, 16384 scattered points each)")
     return ap.parse_args()
@@ -350,6 +352,67 @@ def run_derivs(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- NEXT-4 knot gradients
+def run_knots(args, rank, world):
+    """NEXT-4: nurbs_surface_bwd_knots (control AND true knot gradients) on config 4 / 5,
+    timed beside the plain backward (the knot gradients' extra cost)."""
+    import numpy as np
+    import torch
+
+    import paper_2104_14547_b200 as nb
+    import workloads as wl
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = wl.config4() if args.config == 4 else wl.config5()
+    T_ = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctrl, U, V, u, v = T_(w.ctrl), T_(w.U), T_(w.V), T_(w.u), T_(w.v)
+    sh = nb.nurbs_shape(w.B, w.n, w.m, w.p, w.q, w.n_u, w.n_v, 0)
+    tables = nb.Tables.build(sh, U, V, u, v)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
+    gout = torch.randn((w.B, w.n_u, w.n_v, 3), dtype=torch.float32, device=dev, generator=gen)
+    grad = torch.empty_like(ctrl)
+    gU, gV = torch.empty_like(U), torch.empty_like(V)
+    wsk = nb.knots_workspace_bytes(sh)
+    work = torch.empty(wsk, dtype=torch.uint8, device=dev)
+    wsb = nb.bwd_workspace_bytes(sh)
+    workb = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    kg = lambda: nb.nurbs_surface_bwd_knots(sh, ctrl, U, V, u, v, tables, gout, grad, gU, gV, work, wsk)
+    plain = lambda: nb.nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, gout, grad, gU, gV, workb, wsb)
+
+    def timeit(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    sampler = ClockSampler(local)
+    with sampler:
+        ms = timeit(kg)
+        ms_plain = timeit(plain)
+    pts = w.points
+    byts = pts * 12 + 2 * w.ctrl.nbytes
+    peak, kind = load_peaks()
+    line = {"metric": "NURBS surface points/sec of the backward with true knot gradients (fp32, NEXT-4)",
+            "value": pts / (ms * 1e-3), "unit": "points/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": workload_name(args.config) + " -> dL/dP, dL/dw, dL/dU, dL/dV"},
+            "plain_bwd_ms": ms_plain,
+            "roofline": {"bound": "hbm", "achieved": byts / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": byts / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": byts, "peak_kind": kind},
+            "gpu_launches": args.steps * (7 if wsb == 0 else 8), "clocks": sampler.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------------------- NEXT-1 paired points
 FP32_FMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: FFMA2 fma-pipe peak at clocks.max.sm
 
@@ -482,6 +545,8 @@ def main():
         return run_derivs(args, rank, world)
     if args.paired:
         return run_paired(args, rank, world)
+    if args.knots:
+        return run_knots(args, rank, world)
 
     import torch
     import torch.distributed as dist
