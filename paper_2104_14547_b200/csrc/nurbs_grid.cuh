@@ -74,7 +74,10 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
     for (int k = 0; k <= P; ++k) acc[k] = fma4v(nu[k], G, acc[k]);
     if constexpr (KG) {  // NEXT-4: G . T_r, the row's weight of dN_r/dU
 #pragma unroll
-      for (int k = 0; k <= P; ++k) dots[k] = fmaf(G.x, tw[k].x, fmaf(G.y, tw[k].y, fmaf(G.z, tw[k].z, G.w * tw[k].w)));
+      for (int k = 0; k <= P; ++k) {
+        const float2 t2 = up2(ffma2(pk2(G.z, G.w), pk2(tw[k].z, tw[k].w), fmul2(pk2(G.x, G.y), pk2(tw[k].x, tw[k].y))));
+        dots[k] = t2.x + t2.y;
+      }
     }
   }
 }
@@ -457,19 +460,31 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
 
   // TMA staging: columns >= cols use the unused row tail (the fit step still masks its loss)
   const bool vio = (BULK && !FIT && !KG) ? true : valid;
-  // KG: the warp sums of G . T_r for one walk row -> rowdot[warp][ci][r]
+  // KG: the warp sums of G . T_r for one walk row -> rowdot[warp][ci][r]: a reduce-scatter
+  // over the lanes (fixed butterfly; each of the NVP <= 8 values ends summed in 32/NVP lanes)
   auto kg_row = [&](int ci, const float (&d)[P + 1]) {
     if constexpr (KG) {
-      float x[P + 1];
+      constexpr int NVP = (P + 1) <= 4 ? 4 : 8;
+      float x[NVP];
 #pragma unroll
-      for (int k = 0; k <= P; ++k) x[k] = d[k];
+      for (int k = 0; k < NVP; ++k) x[k] = k <= P ? d[k <= P ? k : 0] : 0.f;
+      int idx = 0;  // which value this lane holds after the scatter levels
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+      for (int half = NVP / 2, o = 16; half > 0; half >>= 1, o >>= 1) {
+        const bool up = (lane & o) != 0;
 #pragma unroll
-        for (int k = 0; k <= P; ++k) x[k] += __shfl_xor_sync(0xffffffffu, x[k], o);
-      if (lane == 0)
+        for (int k = 0; k < half; ++k) {
+          const float send = up ? x[k] : x[k + half];
+          const float keep = up ? x[k + half] : x[k];
+          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        idx += up ? half : 0;
+      }
+      constexpr int LVL = NVP == 4 ? 2 : 3;  // lane bits used by the scatter: 16, 8 (, 4)
+      float v = x[0];
 #pragma unroll
-        for (int k = 0; k <= P; ++k) rowdot[(warp * kRowChunk + ci) * (P + 1) + k] = x[k];
+      for (int o = 16 >> LVL; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((lane & ((16 >> LVL) * 2 - 1)) == 0 && idx <= P) rowdot[(warp * kRowChunk + ci) * (P + 1) + idx] = v;
     }
   };
   // KG: rows [r0, r0 + cn) of the walk are complete in rowdot (after a barrier): warp sums in

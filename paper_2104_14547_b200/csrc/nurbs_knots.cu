@@ -16,21 +16,25 @@
 namespace nb {
 
 // c[t] = sum_r dN_r(u)/dU[s-p+1+t] * h[r], t = 0..2p-1 (A2.2 with dual numbers, one pass per knot).
-template <int MAXD>
-__device__ __forceinline__ void d_basis_dknots(const float* __restrict__ U, int s, float u, int p, const float* h,
-                                               float* c) {
-  float kn[2 * MAXD];  // U[s-p+1 .. s+p]
-  for (int t = 0; t < 2 * p; ++t) kn[t] = __ldg(U + s - p + 1 + t);
-  for (int t = 0; t < 2 * p; ++t) {
-    float N[MAXD + 1], D[MAXD + 1], left[MAXD + 1], right[MAXD + 1], dl[MAXD + 1], dr[MAXD + 1];
+template <int P>
+__device__ __forceinline__ void d_basis_dknots(const float* __restrict__ U, int s, float u, const float (&h)[P + 1],
+                                               float (&c)[2 * P]) {
+  float kn[2 * P];  // U[s-p+1 .. s+p]
+#pragma unroll
+  for (int t = 0; t < 2 * P; ++t) kn[t] = __ldg(U + s - P + 1 + t);
+#pragma unroll
+  for (int t = 0; t < 2 * P; ++t) {
+    float N[P + 1], D[P + 1], left[P + 1], right[P + 1], dl[P + 1], dr[P + 1];
     N[0] = 1.f;
     D[0] = 0.f;
-    for (int j = 1; j <= p; ++j) {
-      left[j] = u - kn[p - j];            // u - U[s+1-j]
-      dl[j] = (p - j == t) ? -1.f : 0.f;
-      right[j] = kn[p - 1 + j] - u;       // U[s+j] - u
-      dr[j] = (p - 1 + j == t) ? 1.f : 0.f;
+#pragma unroll
+    for (int j = 1; j <= P; ++j) {
+      left[j] = u - kn[P - j];            // u - U[s+1-j]
+      dl[j] = (P - j == t) ? -1.f : 0.f;
+      right[j] = kn[P - 1 + j] - u;       // U[s+j] - u
+      dr[j] = (P - 1 + j == t) ? 1.f : 0.f;
       float saved = 0.f, dsaved = 0.f;
+#pragma unroll
       for (int r = 0; r < j; ++r) {
         const float den = right[r + 1] + left[j - r];
         const float dden = dr[r + 1] + dl[j - r];
@@ -47,30 +51,35 @@ __device__ __forceinline__ void d_basis_dknots(const float* __restrict__ U, int 
       D[j] = dsaved;
     }
     float acc = 0.f;
-    for (int r = 0; r <= p; ++r) acc = fmaf(D[r], h[r], acc);
+#pragma unroll
+    for (int r = 0; r <= P; ++r) acc = fmaf(D[r], h[r], acc);
     c[t] = acc;
   }
 }
 
 // Per (surface, sample): h = sum over the nparts partials (ascending), then the 2p knot
 // contributions and the span.
+template <int P>
 __global__ void nurbs_knot_rows_kernel(KnotDir d) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)d.B * d.ns) return;
   const int s = (int)(idx / d.ns), a = (int)(idx - (long long)s * d.ns);
-  const int p = d.p;
-  float h[NURBS_MAXD + 1];
-  for (int r = 0; r <= p; ++r) h[r] = 0.f;
+  float h[P + 1];
+#pragma unroll
+  for (int r = 0; r <= P; ++r) h[r] = 0.f;
   for (int c = 0; c < d.nparts; ++c) {
-    const float* src = d.part + (((size_t)s * d.nparts + c) * d.ns + a) * (p + 1);
-    for (int r = 0; r <= p; ++r) h[r] += src[r];
+    const float* src = d.part + (((size_t)s * d.nparts + c) * d.ns + a) * (P + 1);
+#pragma unroll
+    for (int r = 0; r <= P; ++r) h[r] += src[r];
   }
   const float* Uk = d.knots + (long long)s * d.kstride;
-  int sp = d.tspan ? __ldg(d.tspan + a) : d_find_span(Uk, d.n, p, __ldg(d.samples + a));
-  sp = min(max(sp, p), d.n - 1);
-  float c[2 * NURBS_MAXD];
-  d_basis_dknots<NURBS_MAXD>(Uk, sp, __ldg(d.samples + a), p, h, c);
-  for (int t = 0; t < 2 * p; ++t) d.contrib[(size_t)idx * (2 * p) + t] = c[t];
+  const float ua = __ldg(d.samples + a);
+  int sp = d.tspan ? __ldg(d.tspan + a) : d_find_span(Uk, d.n, P, ua);
+  sp = min(max(sp, P), d.n - 1);
+  float c[2 * P];
+  d_basis_dknots<P>(Uk, sp, ua, h, c);
+#pragma unroll
+  for (int t = 0; t < 2 * P; ++t) d.contrib[(size_t)idx * (2 * P) + t] = c[t];
   d.span[idx] = sp;
 }
 
@@ -119,7 +128,15 @@ cudaError_t launch_knot_grad(const KnotDir& d, bool batched, float* tmp, float* 
   const int nk = d.n + d.p + 1;
   const long long rows = (long long)d.B * d.ns;
   if (d.ns > 0) {
-    nurbs_knot_rows_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(d);
+    const unsigned nbk = (unsigned)((rows + 127) / 128);
+    switch (d.p) {
+      case 1: nurbs_knot_rows_kernel<1><<<nbk, 128, 0, st>>>(d); break;
+      case 2: nurbs_knot_rows_kernel<2><<<nbk, 128, 0, st>>>(d); break;
+      case 3: nurbs_knot_rows_kernel<3><<<nbk, 128, 0, st>>>(d); break;
+      case 4: nurbs_knot_rows_kernel<4><<<nbk, 128, 0, st>>>(d); break;
+      case 5: nurbs_knot_rows_kernel<5><<<nbk, 128, 0, st>>>(d); break;
+      default: return cudaErrorInvalidValue;
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
