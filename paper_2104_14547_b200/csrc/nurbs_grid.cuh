@@ -504,8 +504,8 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   float lsum = 0.f;  // FIT: this thread's sum of |S - T|^2
   // One row of the walk: advance the window to the row's span if it changed (uniform across
   // the CTA, rare: once per knot span), then F2 (+ B1). ci = row index in the smem tables.
-  auto row_step = [&](int ci, float* io, auto flush) {
-    const int target = su_s[ci] - P;
+  auto row_step = [&](int ci, float* io, auto flush, bool chg) {
+    const int target = chg ? su_s[ci] - P : lo;
     if (target != lo) {
       do {  // row lo is complete
         if constexpr (BWD) flush(lo, acc[0]);
@@ -555,10 +555,16 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
     bool fast = nr == RPS;
     if constexpr (BWD) fast = fast && (lo_end - b2_next) <= kHRing;  // ring capacity
     if (fast) {
+      // backward: the rows whose span differs from the previous row's, as one warp-uniform
+      // mask (a ballot), so each unrolled row tests a bit instead of re-reading its span
+      const int rl = min(lane, RPS - 1);
+      const int sp = su_s[ci0 + rl] - P;
+      const int pv = rl == 0 ? lo : su_s[ci0 + rl - 1] - P;
+      const unsigned chg = BWD ? __ballot_sync(0xffffffffu, lane < RPS && sp != pv) : ~0u;
 #pragma unroll
-      for (int r = 0; r < RPS; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_fast);
+      for (int r = 0; r < RPS; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_fast, (chg >> r) & 1u);
     } else {
-      for (int r = 0; r < nr; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_checked);
+      for (int r = 0; r < nr; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_checked, true);
     }
     if constexpr (BWD) {
       while (lo - b2_next >= kB2Batch) {

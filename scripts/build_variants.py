@@ -6,7 +6,13 @@ VARIANTS = {
     "base": [],
     "nob2": ["-DNB_EXP_NO_B2"],
     "b2sync": ["-DNB_EXP_B2_NOSYNC_WORK"],
+    "st2": ["-DNB_STAGES_B=2"],
+    "minb3": ["-DNB_MINB_B=3"],
+    "chunk128": ["-DNB_ROWCHUNK=128"],
+    "st2chunk128": ["-DNB_STAGES_B=2", "-DNB_ROWCHUNK=128"],
+    "rps16st2": ["-DNB_RPS_B=16", "-DNB_STAGES_B=2"],
 }
+os.makedirs("exp", exist_ok=True)
 sel = sys.argv[1:] or list(VARIANTS)
 for name in sel:
     out = os.path.join("exp", f"lib_{name}.so")
