@@ -39,3 +39,4 @@ from .api import (  # noqa: F401
     surface_bwd_knots,
     curve_bwd_knots,
 )
+from .pipeline import HostBatchPipeline  # noqa: F401,E402
