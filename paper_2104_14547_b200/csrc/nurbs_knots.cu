@@ -67,11 +67,23 @@ __global__ void nurbs_knot_rows_kernel(KnotDir d) {
   float h[P + 1];
 #pragma unroll
   for (int r = 0; r <= P; ++r) h[r] = 0.f;
-  for (int c = 0; c < d.nparts; ++c) {
-    const float* src = d.part + (((size_t)s * d.nparts + c) * d.ns + a) * (P + 1);
+  const size_t pstride = (size_t)d.ns * (P + 1);  // between consecutive parts
+  const float* src = d.part + ((size_t)s * d.nparts * d.ns + a) * (P + 1);
+  int pc = 0;
+  for (; pc + 4 <= d.nparts; pc += 4) {  // four parts' loads in flight, added in part order
+    float x[4][P + 1];
 #pragma unroll
-    for (int r = 0; r <= P; ++r) h[r] += src[r];
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r <= P; ++r) x[j][r] = __ldg(src + (size_t)(pc + j) * pstride + r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r <= P; ++r) h[r] += x[j][r];
   }
+  for (; pc < d.nparts; ++pc)
+#pragma unroll
+    for (int r = 0; r <= P; ++r) h[r] += __ldg(src + (size_t)pc * pstride + r);
   const float* Uk = d.knots + (long long)s * d.kstride;
   const float ua = __ldg(d.samples + a);
   int sp = d.tspan ? __ldg(d.tspan + a) : d_find_span(Uk, d.n, P, ua);
@@ -83,12 +95,15 @@ __global__ void nurbs_knot_rows_kernel(KnotDir d) {
   d.span[idx] = sp;
 }
 
-// Per (surface, knot k): sum over the samples whose span window holds k (ascending samples;
-// spans are non-decreasing in the sorted samples, so the window is a contiguous range).
+// Per (surface, knot k): sum over the samples whose span window holds k (spans are
+// non-decreasing in the sorted samples, so the window is a contiguous range). One warp per
+// (surface, knot): lane l sums samples lo+l, lo+l+32, ... in ascending order, then a fixed
+// xor butterfly combines the lanes (deterministic).
 __global__ void nurbs_knot_gather_kernel(KnotDir d, float* out /* [B][nk] */) {
   const int nk = d.n + d.p + 1;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)d.B * nk) return;
+  const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (idx >= (long long)d.B * nk) return;  // warp-uniform
   const int s = (int)(idx / nk), k = (int)(idx - (long long)s * nk);
   const int p = d.p;
   const int* sp = d.span + (size_t)s * d.ns;
@@ -99,11 +114,15 @@ __global__ void nurbs_knot_gather_kernel(KnotDir d, float* out /* [B][nk] */) {
     if (sp[mid] < k - p) lo = mid + 1; else hi = mid;
   }
   float acc = 0.f;
-  for (int a = lo; a < d.ns && sp[a] <= k + p - 1; ++a) {
-    const int t = k - (sp[a] - p + 1);
+  for (int a = lo + lane; a < d.ns; a += 32) {
+    const int spa = sp[a];
+    if (spa > k + p - 1) break;
+    const int t = k - (spa - p + 1);
     if (t >= 0 && t < 2 * p) acc += d.contrib[((size_t)s * d.ns + a) * (2 * p) + t];
   }
-  out[idx] = acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[idx] = acc;
 }
 
 // Shared knots: out[k] = sum over surfaces (fixed partition + fixed tree) of per[s][k].
@@ -123,27 +142,102 @@ __global__ void __launch_bounds__(256) nurbs_knot_sum_kernel(const float* per, i
   if (threadIdx.x == 0) out[k] = red[0];
 }
 
+// Shared knots: the knot derivative of a sample does not depend on the surface, so the
+// per-surface weights h can be summed over the batch first (linearity):
+//   dL/dU_k = sum_a sum_r dN_r(u_a)/dU_k * (sum_s sum_c part[s][c][a][r]).
+// Two fixed-order levels: gpart[g][e] = sum over surfaces [g*B/G, (g+1)*B/G) (ascending) and
+// parts c (ascending); hsum[e] = a fixed tree over the G groups. The per-sample kernels then
+// run once, on one "surface" whose single part is hsum.
+__global__ void nurbs_knot_hgroup_kernel(const float* __restrict__ part, int B, int nparts, int E, int G,
+                                         float* __restrict__ gpart) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)E * G) return;
+  const int g = (int)(idx / E), e = (int)(idx - (long long)g * E);
+  const int s0 = (int)((long long)B * g / G), s1 = (int)((long long)B * (g + 1) / G);
+  const int n = (s1 - s0) * nparts;  // the group's (surface, part) rows, contiguous in part[]
+  const float* src = part + (size_t)s0 * nparts * E + e;
+  float acc = 0.f;
+  int i = 0;
+  for (; i + 4 <= n; i += 4) {  // four independent loads in flight, added in order
+    const float a0 = __ldg(src + (size_t)i * E), a1 = __ldg(src + (size_t)(i + 1) * E);
+    const float a2 = __ldg(src + (size_t)(i + 2) * E), a3 = __ldg(src + (size_t)(i + 3) * E);
+    acc += a0; acc += a1; acc += a2; acc += a3;
+  }
+  for (; i < n; ++i) acc += __ldg(src + (size_t)i * E);
+  gpart[(size_t)g * E + e] = acc;
+}
+
+// hsum[e] = sum over g of gpart[g][e]: one block per element, thread t takes g = t, t+256, ...
+// (ascending), then a fixed shared-memory tree.
+__global__ void __launch_bounds__(256) nurbs_knot_htree_kernel(const float* __restrict__ gpart, int E, int G,
+                                                               float* __restrict__ hsum) {
+  __shared__ float red[256];
+  const int e = blockIdx.x;
+  float a = 0.f;
+  for (int g = threadIdx.x; g < G; g += 256) a += gpart[(size_t)g * E + e];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) hsum[e] = red[0];
+}
+
+static cudaError_t launch_rows(const KnotDir& d, cudaStream_t st) {
+  const long long rows = (long long)d.B * d.ns;
+  const unsigned nbk = (unsigned)((rows + 127) / 128);
+  switch (d.p) {
+    case 1: nurbs_knot_rows_kernel<1><<<nbk, 128, 0, st>>>(d); break;
+    case 2: nurbs_knot_rows_kernel<2><<<nbk, 128, 0, st>>>(d); break;
+    case 3: nurbs_knot_rows_kernel<3><<<nbk, 128, 0, st>>>(d); break;
+    case 4: nurbs_knot_rows_kernel<4><<<nbk, 128, 0, st>>>(d); break;
+    case 5: nurbs_knot_rows_kernel<5><<<nbk, 128, 0, st>>>(d); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_knot_grad(const KnotDir& d, bool batched, float* tmp, float* out, cudaStream_t st) {
   if (d.B == 0) return cudaSuccess;
-  const int nk = d.n + d.p + 1;
-  const long long rows = (long long)d.B * d.ns;
-  if (d.ns > 0) {
-    const unsigned nbk = (unsigned)((rows + 127) / 128);
-    switch (d.p) {
-      case 1: nurbs_knot_rows_kernel<1><<<nbk, 128, 0, st>>>(d); break;
-      case 2: nurbs_knot_rows_kernel<2><<<nbk, 128, 0, st>>>(d); break;
-      case 3: nurbs_knot_rows_kernel<3><<<nbk, 128, 0, st>>>(d); break;
-      case 4: nurbs_knot_rows_kernel<4><<<nbk, 128, 0, st>>>(d); break;
-      case 5: nurbs_knot_rows_kernel<5><<<nbk, 128, 0, st>>>(d); break;
-      default: return cudaErrorInvalidValue;
+  if (!batched && d.B >= 16 && d.ns > 0) {
+    // workspace (d.contrib holds B*ns*2p floats): [G][ns][p+1] group sums, [ns][p+1] batch
+    // sum, then the one surface's [ns][2p] contributions
+    const int E = d.ns * (d.p + 1);
+    const long long cap = (long long)d.B * d.ns * 2 * d.p;
+    long long G = (cap - (long long)d.ns * 2 * d.p - E) / E;
+    G = G > 256 ? 256 : G;
+    G = G > d.B ? d.B : G;
+    if (G >= 1) {
+      float* gpart = d.contrib;
+      float* hsum = gpart + (size_t)G * E;
+      const long long th = (long long)E * G;
+      nurbs_knot_hgroup_kernel<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(d.part, d.B, d.nparts, E, (int)G, gpart);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      nurbs_knot_htree_kernel<<<(unsigned)E, 256, 0, st>>>(gpart, E, (int)G, hsum);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      KnotDir d1 = d;
+      d1.B = 1;
+      d1.kstride = 0;
+      d1.part = hsum;
+      d1.nparts = 1;
+      d1.contrib = hsum + E;
+      if ((e = launch_rows(d1, st)) != cudaSuccess) return e;
+      const int nk = d.n + d.p + 1;
+      nurbs_knot_gather_kernel<<<(unsigned)((nk * 32LL + 127) / 128), 128, 0, st>>>(d1, out);
+      return cudaGetLastError();
     }
-    cudaError_t e = cudaGetLastError();
+  }
+  const int nk = d.n + d.p + 1;
+  if (d.ns > 0) {
+    cudaError_t e = launch_rows(d, st);
     if (e != cudaSuccess) return e;
   }
   float* dst = batched ? out : tmp;
   const long long items = (long long)d.B * nk;
   if (d.ns > 0) {
-    nurbs_knot_gather_kernel<<<(unsigned)((items + 127) / 128), 128, 0, st>>>(d, dst);
+    nurbs_knot_gather_kernel<<<(unsigned)((items * 32 + 127) / 128), 128, 0, st>>>(d, dst);
   } else {
     cudaError_t e = cudaMemsetAsync(dst, 0, sizeof(float) * (size_t)items, st);
     if (e != cudaSuccess) return e;

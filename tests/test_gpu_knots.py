@@ -64,6 +64,14 @@ def test_knot_grad_parity_degrees(p, q, batched):
     check(w)
 
 
+@pytest.mark.parametrize("B,p,q,n_v", [(16, 3, 3, 29), (40, 2, 5, 150), (23, 4, 1, 300)])
+def test_knot_grad_shared_knots_batch_first_sum(B, p, q, n_v):
+    """Shared knots with B >= 16: the assembly sums the per-surface weights over the batch
+    first (two-level fixed tree) and differentiates once; against the oracle's batch sum."""
+    w = wl.surfaces(f"kb{B}", B, 9, 11, p, q, 37, n_v, seed=B + p)
+    check(w)
+
+
 def test_knot_grad_tiled_and_tables():
     """Several row and column blocks (the reduce path, several partials per sample)."""
     w = wl.surfaces("tiled", 1, 12, 10, 3, 3, 50, 260, seed=8)   # NRB = 9 row blocks, NCB = 3
