@@ -9,6 +9,8 @@
 #include <cstring>
 #include <string>
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
+
 #include "../../include/nurbs.h"
 #include "nurbs_internal.cuh"
 #include "nurbs_points.cuh"
@@ -111,6 +113,40 @@ void attach_tables(Geo& g, const void* tables) {
   g.c.tnp = L.np_c;
 }
 
+// ---- 2-D TMA descriptor of a streamed [rows][n_v][3] fp32 tensor (out, dL/dS or the fit
+// target), box = rps rows x 64 sample columns. Used when a stage's rows are not contiguous
+// (n_v != 128); else (or if the driver entry point is unavailable) the kernels keep their
+// bulk-copy paths.
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+void set_io_map(nb::Params& prm, const float* base, long long rows, int nv, int rps) {
+  prm.tmap = 0;
+  if (!prm.bulk || nv < nb::kBoxCols || (nv == nb::kCB && prm.NCB == 1) || rows <= 0) return;
+  PFN_cuTensorMapEncodeTiled_v12000 fn = tmap_encoder();
+  if (!fn) return;
+  const cuuint64_t dims[2] = {(cuuint64_t)nv * 3, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)nv * 12};
+  const cuuint32_t box[2] = {3 * nb::kBoxCols, (cuuint32_t)rps};
+  const cuuint32_t es[2] = {1, 1};
+  if (fn(&prm.io_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+    prm.tmap = 1;
+}
+
 // Checked mode: validate data on the device and synchronize.
 int validate_geo(const Geo& g, const float* ctrl, cudaStream_t st) {
   unsigned long long* d = nullptr;
@@ -180,6 +216,7 @@ int launch(const Geo& g, bool bwd, const float* ctrl, float* out, const float* g
     prm.slots = reinterpret_cast<float4*>(ws);
     prm.colband = reinterpret_cast<int2*>(static_cast<unsigned char*>(ws) + pl.slots_bytes);
   }
+  set_io_map(prm, bwd ? gout : out, (long long)g.B * g.r.ns, g.c.ns, bwd ? nb::kRPS_B : nb::kRPS_F);
   cudaError_t e = nb::launch_grid(prm, bwd ? 1 : 0, g.P, g.c.p, st);
   if (e != cudaSuccess) return cuda_fail(e, bwd ? "backward kernel launch" : "forward kernel launch");
   if (bwd && !pl.direct) {
@@ -229,6 +266,7 @@ int launch_fit(const Geo& g, float* ctrl, const float* target, float lr, float* 
   prm.ctrl_mut = reinterpret_cast<float4*>(ctrl);
   prm.lr = lr;
   prm.fit_scale = (float)(2.0 / ((double)g.B * g.r.ns * g.c.ns));
+  set_io_map(prm, target, (long long)g.B * g.r.ns, g.c.ns, nb::kRPS_B);
   cudaError_t e = nb::launch_grid(prm, 2, g.P, g.c.p, st);
   if (e != cudaSuccess) return cuda_fail(e, "fit kernel launch");
   e = nb::launch_fit_update(prm, g.P, st);
@@ -306,6 +344,7 @@ int launch_knots(const Geo& g, const float* ctrl, const float* gout, float* gctr
   }
   prm.hU = reinterpret_cast<float*>(w + W.hU);
   prm.hV = reinterpret_cast<float*>(w + W.hV);
+  set_io_map(prm, gout, (long long)g.B * g.r.ns, g.c.ns, nb::kRPS_B);
   cudaError_t e = nb::launch_grid(prm, 3, g.P, g.c.p, st);
   if (e != cudaSuccess) return cuda_fail(e, "backward (knot gradients) kernel launch");
   if (!pl.direct && (e = nb::launch_reduce(prm, g.P, st)) != cudaSuccess) return cuda_fail(e, "reduce kernel launch");

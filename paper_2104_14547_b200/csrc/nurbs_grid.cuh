@@ -199,8 +199,13 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
   __syncthreads();  // ring slots free again
 }
 
-template <int P, int Q, bool BWD, bool BULK, bool FIT, bool KG>
-__global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) nurbs_grid_kernel(const Params prm) {
+// IO: how the streamed tensor (out / dL/dS / target) moves: 0 per-thread global accesses,
+// 1 TMA bulk copies (one per stage when rows are contiguous, else one per row), 2 2-D TMA
+// tensor copies (two boxes per stage; rows need not be contiguous).
+template <int P, int Q, bool BWD, int IO, bool FIT, bool KG>
+__global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
+    nurbs_grid_kernel(const __grid_constant__ Params prm) {
+  constexpr bool BULK = IO >= 1;
   static_assert(!FIT || BWD, "the fitting step is a backward variant");
   static_assert(!KG || (BWD && !FIT), "knot gradients extend the plain backward");
   extern __shared__ __align__(128) unsigned char smem[];
@@ -234,7 +239,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
 
   // ---- shared memory carve-up (sizes: grid_smem_bytes)
   float4* cband = reinterpret_cast<float4*>(smem);                                 // [T_rows][CBW]
-  float* stage = reinterpret_cast<float*>(cband + (size_t)prm.T_rows * prm.CBW);    // [NST][RPS][SROW]
+  // [NST] slots of RPS rows: row-major [RPS][SROW], or with the tensor map two column halves
+  // [2][RPS][3*kBoxCols] (each half is one dense TMA box); 128-byte aligned
+  float* stage = reinterpret_cast<float*>(smem + (((size_t)prm.T_rows * prm.CBW * 16 + 127) & ~(size_t)127));
   float4* Hring = reinterpret_cast<float4*>(stage + NST * RPS * SROW);              // [kHRing][kCB] (bwd)
   int* su_s = reinterpret_cast<int*>(Hring + (BWD ? kHRing * kCB : 0));            // [kRowChunk]
   float* Nu_s = reinterpret_cast<float*>(su_s + kRowChunk);                        // [kRowChunk][NP]
@@ -310,28 +317,67 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   // the LAST warp to finish a stage (smem counter) issues the TMA for it — the next dL/dS
   // load into the freed slot (bwd) or the drain of the filled slot to HBM (fwd).
   const uint32_t rowbytes = (uint32_t)cols * 12u;
+#ifdef NB_EXP_ROWCOPIES
+  const bool one_copy = false;
+#else
   const bool one_copy = (cols == C.ns) && cols == kCB;  // a stage is one contiguous span
+#endif
   const size_t grow = (size_t)C.ns * 3;                 // floats between consecutive rows
   const size_t g0 = (((size_t)s * R.ns + a_lo) * C.ns + B0) * 3;  // row a_lo, column B0
+  // tensor-map path: column halves h = 0, 1 of the block (64 sample columns each), rows of the
+  // flattened [B*n_u] row index; a partial last stage falls back to per-row copies (a full box
+  // would touch the next tile's rows)
+  constexpr bool tm = IO == 2;
+  constexpr int HROW = 3 * kBoxCols;                    // floats of one row of a half
+  const int nh = cols > kBoxCols ? 2 : 1;               // halves holding columns of this block
+  const uint32_t hb0 = (uint32_t)min(cols, kBoxCols) * 12u, hb1 = (uint32_t)max(0, cols - kBoxCols) * 12u;
+  const int ty0 = s * R.ns + a_lo;                      // tensor row of walk row 0
+  // this thread's 3 floats of a staged row, and the distance between staged rows
+  const int io_off = tm ? (tid >> 6) * (RPS * HROW) + (tid & 63) * 3 : tid * 3;
+  constexpr size_t io_stride = tm ? (size_t)HROW : (size_t)SROW;
   auto issue_load = [&](int k, int slot) {  // bwd, one thread: stage k of dL/dS into `slot`
     const int nr = min(RPS, nwalk - k * RPS);
     float* buf = stage + slot * (RPS * SROW);
     const float* src = prm.gout + g0 + (size_t)k * RPS * grow;
-    mbar_arrive_expect_tx(sfull + slot, rowbytes * nr);
-    if (one_copy) {
-      bulk_g2s(buf, src, rowbytes * nr, sfull + slot);
+    if constexpr (tm) {
+      if (nr == RPS) {
+        mbar_arrive_expect_tx(sfull + slot, (uint32_t)nh * RPS * HROW * 4u);
+        for (int h = 0; h < nh; ++h) tma_load_2d(buf + h * RPS * HROW, &prm.io_map, 3 * (B0 + h * kBoxCols), ty0 + k * RPS, sfull + slot);
+      } else {
+        mbar_arrive_expect_tx(sfull + slot, (hb0 + hb1) * nr);
+        for (int rr = 0; rr < nr; ++rr) {
+          bulk_g2s(buf + rr * HROW, src + (size_t)rr * grow, hb0, sfull + slot);
+          if (hb1) bulk_g2s(buf + RPS * HROW + rr * HROW, src + (size_t)rr * grow + HROW, hb1, sfull + slot);
+        }
+      }
     } else {
-      for (int rr = 0; rr < nr; ++rr) bulk_g2s(buf + rr * SROW, src + (size_t)rr * grow, rowbytes, sfull + slot);
+      mbar_arrive_expect_tx(sfull + slot, rowbytes * nr);
+      if (one_copy) {
+        bulk_g2s(buf, src, rowbytes * nr, sfull + slot);
+      } else {
+        for (int rr = 0; rr < nr; ++rr) bulk_g2s(buf + rr * SROW, src + (size_t)rr * grow, rowbytes, sfull + slot);
+      }
     }
   };
   auto issue_store = [&](int k, int slot) {  // fwd, one thread: drain stage k from `slot`
     const int nr = min(RPS, nwalk - k * RPS);
     const float* buf = stage + slot * (RPS * SROW);
     float* dst = prm.out + g0 + (size_t)k * RPS * grow;
-    if (one_copy) {
-      bulk_s2g(dst, buf, rowbytes * nr);
+    if constexpr (tm) {
+      if (nr == RPS) {
+        for (int h = 0; h < nh; ++h) tma_store_2d(&prm.io_map, 3 * (B0 + h * kBoxCols), ty0 + k * RPS, buf + h * RPS * HROW);
+      } else {
+        for (int rr = 0; rr < nr; ++rr) {
+          bulk_s2g(dst + (size_t)rr * grow, buf + rr * HROW, hb0);
+          if (hb1) bulk_s2g(dst + (size_t)rr * grow + HROW, buf + RPS * HROW + rr * HROW, hb1);
+        }
+      }
     } else {
-      for (int rr = 0; rr < nr; ++rr) bulk_s2g(dst + (size_t)rr * grow, buf + rr * SROW, rowbytes);
+      if (one_copy) {
+        bulk_s2g(dst, buf, rowbytes * nr);
+      } else {
+        for (int rr = 0; rr < nr; ++rr) bulk_s2g(dst + (size_t)rr * grow, buf + rr * SROW, rowbytes);
+      }
     }
     bulk_commit();
     bulk_wait_read_all();  // the slot may be rewritten once TMA has read it
@@ -618,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
       float* sslot = stage + slot * (RPS * SROW);
       if constexpr (BWD) mbar_wait(sfull + slot, use & 1);
       else if (use > 0) mbar_wait(sempty + slot, (use - 1) & 1);
-      run_rows(ci0, nr, sslot + tid * 3, SROW);
+      run_rows(ci0, nr, sslot + io_off, io_stride);
       if constexpr (!BWD) fence_proxy_async();  // this thread's staged rows -> async proxy
       __syncwarp();
       if (lane == 0) {
@@ -676,29 +722,35 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F) n
   }
 }
 
-template <int P, int Q, bool BWD, bool BULK, bool FIT, bool KG = false>
+template <int P, int Q, bool BWD, int IO, bool FIT, bool KG = false>
 static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
   const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows, prm.CBW, KG);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, BULK, FIT, KG>,
+    cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, IO, FIT, KG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  nurbs_grid_kernel<P, Q, BWD, BULK, FIT, KG>
+  nurbs_grid_kernel<P, Q, BWD, IO, FIT, KG>
       <<<(unsigned)((long long)prm.B * prm.NRB * prm.NCB), kThreads, smem, st>>>(prm);
   return cudaGetLastError();
 }
 
 // mode: 0 forward, 1 backward, 2 fused fitting step (backward with dL/dS from a target),
 // 3 backward with the knot-gradient partials (NEXT-4)
+template <int P, int Q, int IO>
+static cudaError_t launch_pq_io(const Params& prm, int mode, cudaStream_t st) {
+  if (mode == 3) return launch_one<P, Q, true, IO, false, true>(prm, st);
+  if (mode == 2) return launch_one<P, Q, true, IO, true>(prm, st);
+  if (mode == 1) return launch_one<P, Q, true, IO, false>(prm, st);
+  return launch_one<P, Q, false, IO, false>(prm, st);
+}
 template <int P, int Q>
 static cudaError_t launch_pq(const Params& prm, int mode, cudaStream_t st) {
-  if (mode == 3) return prm.bulk ? launch_one<P, Q, true, true, false, true>(prm, st) : launch_one<P, Q, true, false, false, true>(prm, st);
-  if (mode == 2) return prm.bulk ? launch_one<P, Q, true, true, true>(prm, st) : launch_one<P, Q, true, false, true>(prm, st);
-  if (mode == 1) return prm.bulk ? launch_one<P, Q, true, true, false>(prm, st) : launch_one<P, Q, true, false, false>(prm, st);
-  return prm.bulk ? launch_one<P, Q, false, true, false>(prm, st) : launch_one<P, Q, false, false, false>(prm, st);
+  if (prm.bulk && prm.tmap) return launch_pq_io<P, Q, 2>(prm, mode, st);
+  if (prm.bulk) return launch_pq_io<P, Q, 1>(prm, mode, st);
+  return launch_pq_io<P, Q, 0>(prm, mode, st);
 }
 
 template <int P>

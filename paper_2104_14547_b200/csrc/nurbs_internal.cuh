@@ -7,6 +7,7 @@
 // one sample) and the curve along the columns.
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (the TMA descriptor type; no driver-library link needed)
 #include <cuda_runtime.h>
 
 namespace nb {
@@ -101,7 +102,14 @@ struct Params {
   // true knot gradients (NEXT-4, mode 3)
   float* hU;                // [B][NCB][r.ns][P+1]: sum over the block's columns of G . T_r
   float* hV;                // [B][NRB][c.ns][q+1]: sum over the band rows of Q[i][sv-q+h] . H[i][b]
+  // 2-D TMA descriptor of the streamed tensor (out in the forward, dL/dS or the target in the
+  // backward / fitting step) viewed as [B*n_u rows][n_v*3 floats], box = RPS rows x 192 floats
+  // (64 sample columns): one stage of a 128-column block moves in two tensor copies instead of
+  // one bulk copy per row. tmap == 0: per-row bulk copies (or one copy when rows are contiguous).
+  int tmap;
+  CUtensorMap io_map;       // 64-byte aligned; read through the kernel's __grid_constant__ params
 };
+constexpr int kBoxCols = 64;             // sample columns per tensor box (192 floats)
 
 // Tables blob layout (nurbs_tables): header then four arrays, each 256-byte aligned.
 struct TabLayout {

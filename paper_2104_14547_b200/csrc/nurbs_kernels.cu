@@ -144,7 +144,7 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg) {
   const int NP = (P + 1) <= 4 ? 4 : 8;
   const int NQ = (q + 1) <= 4 ? 4 : 8;
   const int rps = bwd ? kRPS_B : kRPS_F, nst = bwd ? kStages_B : kStages_F;
-  size_t b = (size_t)T_rows * CBW * 16 + (size_t)nst * rps * kCB * 3 * 4 + kRowChunk * 4 +
+  size_t b = (((size_t)T_rows * CBW * 16 + 127) & ~(size_t)127) + (size_t)nst * rps * kCB * 3 * 4 + kRowChunk * 4 +
              (size_t)kRowChunk * NP * 4;
   if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4 + (kCB + 4) * 4;
   b += 4 * 4;                                  // misc

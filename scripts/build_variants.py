@@ -4,13 +4,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2104_14547_b200.build import build
 VARIANTS = {
     "base": [],
+    "rowcopies": ["-DNB_EXP_ROWCOPIES"],
     "nob2": ["-DNB_EXP_NO_B2"],
     "b2sync": ["-DNB_EXP_B2_NOSYNC_WORK"],
     "st2": ["-DNB_STAGES_B=2"],
     "minb3": ["-DNB_MINB_B=3"],
     "chunk128": ["-DNB_ROWCHUNK=128"],
-    "st2chunk128": ["-DNB_STAGES_B=2", "-DNB_ROWCHUNK=128"],
-    "rps16st2": ["-DNB_RPS_B=16", "-DNB_STAGES_B=2"],
+    "f_r4s4": ["-DNB_RPS_F=4", "-DNB_STAGES_F=4"],
+    "f_r4s3": ["-DNB_RPS_F=4", "-DNB_STAGES_F=3"],
+    "f_r8s3": ["-DNB_STAGES_F=3"],
+    "f_r2s6": ["-DNB_RPS_F=2", "-DNB_STAGES_F=6"],
 }
 os.makedirs("exp", exist_ok=True)
 sel = sys.argv[1:] or list(VARIANTS)
