@@ -526,31 +526,31 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
 
   // TMA staging: columns >= cols use the unused row tail (the fit step still masks its loss)
   const bool vio = (BULK && !FIT && !KG) ? true : valid;
-  // KG: the warp sums of G . T_r for one walk row -> rowdot[warp][ci][r]: a reduce-scatter
-  // over the lanes (fixed butterfly; each of the NVP <= 8 values ends summed in 32/NVP lanes)
+  // KG: the warp sums of G . T_r per walk row -> rowdot[warp][ci][r]. Each lane parks its
+  // p+1 dot products of the stage's rows in a per-warp buffer (row stride 33 floats: the
+  // column reads below are bank-conflict free); at the end of the stage lane l sums one
+  // (row, r) pair over the 32 lanes in lane order (deterministic) — no per-row shuffles.
+  constexpr int KGS = 33;
+  float* kgb = rowdot + (kThreads / 32) * kRowChunk * (P + 1) + warp * (RPS * (P + 1) * KGS);
   auto kg_row = [&](int ci, const float (&d)[P + 1]) {
     if constexpr (KG) {
-      constexpr int NVP = (P + 1) <= 4 ? 4 : 8;
-      float x[NVP];
+      const int rr = ci % RPS;
 #pragma unroll
-      for (int k = 0; k < NVP; ++k) x[k] = k <= P ? d[k <= P ? k : 0] : 0.f;
-      int idx = 0;  // which value this lane holds after the scatter levels
-#pragma unroll
-      for (int half = NVP / 2, o = 16; half > 0; half >>= 1, o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int k = 0; k < half; ++k) {
-          const float send = up ? x[k] : x[k + half];
-          const float keep = up ? x[k + half] : x[k];
-          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-        idx += up ? half : 0;
+      for (int k = 0; k <= P; ++k) kgb[(rr * (P + 1) + k) * KGS + lane] = d[k];
+    }
+  };
+  auto kg_stage = [&](int ci0, int nr) {
+    if constexpr (KG) {
+      __syncwarp();
+      for (int pr = lane; pr < nr * (P + 1); pr += 32) {
+        const float* src = kgb + pr * KGS;
+        float v = 0.f;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) v += src[j];
+        const int rr = pr / (P + 1), k = pr - rr * (P + 1);
+        rowdot[(warp * kRowChunk + ci0 + rr) * (P + 1) + k] = v;
       }
-      constexpr int LVL = NVP == 4 ? 2 : 3;  // lane bits used by the scatter: 16, 8 (, 4)
-      float v = x[0];
-#pragma unroll
-      for (int o = 16 >> LVL; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if ((lane & ((16 >> LVL) * 2 - 1)) == 0 && idx <= P) rowdot[(warp * kRowChunk + ci) * (P + 1) + idx] = v;
+      __syncwarp();
     }
   };
   // KG: rows [r0, r0 + cn) of the walk are complete in rowdot (after a barrier): warp sums in
@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
     } else {
       run_rows(ci0, nr, gio + (size_t)r0 * grow, grow);
     }
+    kg_stage(ci0, nr);
     if (++slot == NST) { slot = 0; ++use; }
   }
   if constexpr (BULK && !BWD) bulk_wait_all();  // every store this thread issued has landed

@@ -150,7 +150,8 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg, boo
   if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4 + (kCB + 4) * 4;
   b += 4 * 4;                                  // misc
   b = (b + 7) / 8 * 8 + (1 + 2 * nst) * 8 + nst * 4;  // mbarriers + stage counters
-  if (kg) b += 8 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4;  // rowdot (NEXT-4)
+  if (kg)  // rowdot + the per-warp stage buffers of the row dot products (NEXT-4)
+    b += 8 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4 + (size_t)(kThreads / 32) * kRPS_B * (P + 1) * 33 * 4;
   return b;
 }
 
