@@ -158,17 +158,19 @@ def test_ragged_columns_and_non_tma_path(n_v):
     check_surface(w)
 
 
-@pytest.mark.parametrize("n_u,n_v", [(45, 64), (13, 196), (70, 132), (9, 256), (37, 324)])
-def test_tensor_map_path(n_u, n_v, monkeypatch):
+@pytest.mark.parametrize("n_u,n_v,tables", [(45, 64, False), (13, 196, True), (70, 132, False), (9, 256, False),
+                                             (37, 324, True), (200, 68, True)])
+def test_tensor_map_path(n_u, n_v, tables, monkeypatch):
     """n_v % 4 == 0 and rows not contiguous per stage: the 2-D TMA tensor path (two 64-column
-    boxes per 8-row stage, per-row fallback for a partial last stage, ragged second box).
-    Against the oracle, and bitwise against the per-thread (non-TMA) path."""
+    boxes per 8-row stage, per-row fallback for a partial last stage, ragged second box; with
+    tables the forward's cp.async row-table prefetch over several 64-row chunks). Against the
+    oracle, and bitwise against the per-thread (non-TMA) path."""
     w = wl.surfaces("tmap", B=2, n=11, m=9, p=3, q=3, n_u=n_u, n_v=n_v, seed=n_u + n_v)
-    check_surface(w)
+    check_surface(w, tables=tables)
     g = w.grad_out(2)
-    a = run_surface(w, g)
+    a = run_surface(w, g, tables)
     monkeypatch.setenv("NURBS_NO_TMA", "1")
-    b = run_surface(w, g)
+    b = run_surface(w, g, tables)
     np.testing.assert_array_equal(a[0], b[0])
     np.testing.assert_array_equal(a[1], b[1])
 
