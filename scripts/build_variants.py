@@ -5,6 +5,8 @@ from paper_2104_14547_b200.build import build
 VARIANTS = {
     "base": [],
     "rowcopies": ["-DNB_EXP_ROWCOPIES"],
+    "t8192": ["-DNB_TARGET_CTAS=8192"],
+    "t1184": ["-DNB_TARGET_CTAS=1184"],
     "nob2": ["-DNB_EXP_NO_B2"],
     "b2sync": ["-DNB_EXP_B2_NOSYNC_WORK"],
     "st2": ["-DNB_STAGES_B=2"],
