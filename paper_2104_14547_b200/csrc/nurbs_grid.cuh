@@ -212,7 +212,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
   constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
   constexpr int RPS = BWD ? kRPS_B : kRPS_F;      // sample rows per pipeline stage
-  constexpr int NST = BWD ? kStages_B : kStages_F;  // stages per warp ring
+  // stages per ring (the knot-gradient variant runs 2 so that, with its dot-product buffers,
+  // four CTAs still fit an SM)
+  constexpr int NST = BWD ? (KG ? 2 : kStages_B) : kStages_F;
   constexpr int SROW = kCB * 3;                    // floats of one staged sample row
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -530,11 +532,11 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
   // p+1 dot products of the stage's rows in a per-warp buffer (row stride 33 floats: the
   // column reads below are bank-conflict free); at the end of the stage lane l sums one
   // (row, r) pair over the 32 lanes in lane order (deterministic) — no per-row shuffles.
-  constexpr int KGS = 33;
-  float* kgb = rowdot + (kThreads / 32) * kRowChunk * (P + 1) + warp * (RPS * (P + 1) * KGS);
+  constexpr int KGS = 33, KGR = 4;  // buffer row stride, rows per buffer fill
+  float* kgb = rowdot + (kThreads / 32) * kRowChunk * (P + 1) + warp * (KGR * (P + 1) * KGS);
   auto kg_row = [&](int ci, const float (&d)[P + 1]) {
     if constexpr (KG) {
-      const int rr = ci % RPS;
+      const int rr = ci % KGR;
 #pragma unroll
       for (int k = 0; k <= P; ++k) kgb[(rr * (P + 1) + k) * KGS + lane] = d[k];
     }
@@ -615,6 +617,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
         float dots[P + 1];
         walk_row<P, BWD, FIT, KG>(nu, tw, acc, io0 + r * io_stride, vio, fit_scale, lsum, dots);
         kg_row(ci0 + r, dots);
+        if ((r + 1) % KGR == 0) kg_stage(ci0 + r + 1 - KGR, KGR);
       }
       return;
     }
@@ -628,9 +631,15 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
       const int pv = rl == 0 ? lo : su_s[ci0 + rl - 1] - P;
       const unsigned chg = BWD ? __ballot_sync(0xffffffffu, lane < RPS && sp != pv) : ~0u;
 #pragma unroll
-      for (int r = 0; r < RPS; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_fast, (chg >> r) & 1u);
+      for (int r = 0; r < RPS; ++r) {
+        row_step(ci0 + r, io0 + r * io_stride, flush_fast, (chg >> r) & 1u);
+        if ((r + 1) % KGR == 0) kg_stage(ci0 + r + 1 - KGR, KGR);
+      }
     } else {
-      for (int r = 0; r < nr; ++r) row_step(ci0 + r, io0 + r * io_stride, flush_checked, true);
+      for (int r = 0; r < nr; ++r) {
+        row_step(ci0 + r, io0 + r * io_stride, flush_checked, true);
+        if ((r + 1) % KGR == 0 || r == nr - 1) kg_stage(ci0 + r / KGR * KGR, r % KGR + 1);
+      }
     }
     if constexpr (BWD) {
       while (lo - b2_next >= kB2Batch) {
@@ -711,7 +720,6 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
     } else {
       run_rows(ci0, nr, gio + (size_t)r0 * grow, grow);
     }
-    kg_stage(ci0, nr);
     if (++slot == NST) { slot = 0; ++use; }
   }
   if constexpr (BULK && !BWD) bulk_wait_all();  // every store this thread issued has landed

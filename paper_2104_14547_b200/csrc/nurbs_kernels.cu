@@ -143,7 +143,7 @@ __global__ void nurbs_validate_kernel(int B, Dir R, Dir C, int check_rows, const
 size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg, bool tmap) {
   const int NP = (P + 1) <= 4 ? 4 : 8;
   const int NQ = (q + 1) <= 4 ? 4 : 8;
-  const int rps = bwd ? kRPS_B : kRPS_F, nst = bwd ? kStages_B : kStages_F;
+  const int rps = bwd ? kRPS_B : kRPS_F, nst = bwd ? (kg ? 2 : kStages_B) : kStages_F;
   const int nrt = tmap && P > 0 && !bwd ? 2 : 1;  // row tables double-buffered (tensor-map forward)
   size_t b = (((size_t)T_rows * CBW * 16 + 127) & ~(size_t)127) + (size_t)nst * rps * kCB * 3 * 4 + nrt * kRowChunk * 4 +
              (size_t)nrt * kRowChunk * NP * 4;
@@ -151,7 +151,7 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg, boo
   b += 4 * 4;                                  // misc
   b = (b + 7) / 8 * 8 + (1 + 2 * nst) * 8 + nst * 4;  // mbarriers + stage counters
   if (kg)  // rowdot + the per-warp stage buffers of the row dot products (NEXT-4)
-    b += 8 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4 + (size_t)(kThreads / 32) * kRPS_B * (P + 1) * 33 * 4;
+    b += 8 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4 + (size_t)(kThreads / 32) * 4 * (P + 1) * 33 * 4;
   return b;
 }
 
