@@ -49,13 +49,34 @@ __global__ void __launch_bounds__(256) nurbs_reduce_kernel(const Params prm, int
         const int mid = (lo + hi) >> 1;
         if (cbands[mid].y < j) lo = mid + 1; else hi = mid;
       }
+      int cb_hi = lo;  // one past the last column block whose band contains j
+      while (cb_hi < prm.NCB && cbands[cb_hi].x <= j) ++cb_hi;
+      const int nrb = rb_hi - rb_lo + 1, ncb = cb_hi - lo;
+      const float4* sl = prm.slots + (((size_t)s * prm.NRB) * prm.NCB) * prm.T_rows * m + j;
+      auto slot = [&](int rb, int cb) {
+        return sl + (((size_t)rb * prm.NCB + cb) * prm.T_rows + (i - rb * K)) * m;
+      };
       float4 a4 = f4(0.f);
-      for (int rb = rb_lo; rb <= rb_hi; ++rb) {
-        const int r = i - rb * K;
-        for (int cb = lo; cb < prm.NCB && cbands[cb].x <= j; ++cb) {
-          const float4 v = prm.slots[((((size_t)s * prm.NRB + rb) * prm.NCB + cb) * prm.T_rows + r) * m + j];
-          a4.x += v.x; a4.y += v.y; a4.z += v.z; a4.w += v.w;
-        }
+      constexpr int RBX = kMaxQ + 1, CBX = 2;  // the common case: every load issued before the sums
+      if (nrb <= RBX && ncb <= CBX) {
+        float4 v[RBX][CBX];
+#pragma unroll
+        for (int u = 0; u < RBX; ++u)
+#pragma unroll
+          for (int w = 0; w < CBX; ++w) v[u][w] = (u < nrb && w < ncb) ? *slot(rb_lo + u, lo + w) : f4(0.f);
+#pragma unroll
+        for (int u = 0; u < RBX; ++u)  // rb ascending, then cb ascending (the fixed order)
+#pragma unroll
+          for (int w = 0; w < CBX; ++w)
+            if (u < nrb && w < ncb) {
+              a4.x += v[u][w].x; a4.y += v[u][w].y; a4.z += v[u][w].z; a4.w += v[u][w].w;
+            }
+      } else {
+        for (int rb = rb_lo; rb <= rb_hi; ++rb)
+          for (int cb = lo; cb < cb_hi; ++cb) {
+            const float4 v = *slot(rb, cb);
+            a4.x += v.x; a4.y += v.y; a4.z += v.z; a4.w += v.w;
+          }
       }
       // epilogue (Eq.8/9): dP = w dQ_xyz, dw = P.dQ_xyz + dQ_w
       g = make_float4(c.w * a4.x, c.w * a4.y, c.w * a4.z, fmaf(c.x, a4.x, fmaf(c.y, a4.y, fmaf(c.z, a4.z, a4.w))));
