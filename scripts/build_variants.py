@@ -6,9 +6,8 @@ VARIANTS = {
     "base": [],
     "rowcopies": ["-DNB_EXP_ROWCOPIES"],
     "t8192": ["-DNB_TARGET_CTAS=8192"],
-    "cpt1": ["-DNB_CPT2=0"],
-    "cpt2st2": ["-DNB_STAGES_B=2"],
-    "cpt2st2m6": ["-DNB_STAGES_B=2", "-DNB_MINB_B=6"],
+    "xvec": ["--extra-device-vectorization"],
+    "expopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "t1184": ["-DNB_TARGET_CTAS=1184"],
     "nob2": ["-DNB_EXP_NO_B2"],
     "b2sync": ["-DNB_EXP_B2_NOSYNC_WORK"],
