@@ -118,17 +118,17 @@ void attach_tables(Geo& g, const void* tables) {
 // (n_v != 128); else (or if the driver entry point is unavailable) the kernels keep their
 // bulk-copy paths.
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // resolved once (thread-safe static initialisation); nullptr if the driver lacks it
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
     if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+      f = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     cudaGetLastError();
-  }
+    return f;
+  }();
   return fn;
 }
 

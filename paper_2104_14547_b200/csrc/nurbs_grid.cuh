@@ -762,12 +762,16 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
 template <int P, int Q, bool BWD, int IO, bool FIT, bool KG = false>
 static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
   const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows, prm.CBW, KG, IO == 2);
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the dynamic shared-memory opt-in is per device (a benign race: setting it twice is harmless)
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaError_t e0 = cudaGetDevice(&dev);
+  if (e0 != cudaSuccess) return e0;
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(nurbs_grid_kernel<P, Q, BWD, IO, FIT, KG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   nurbs_grid_kernel<P, Q, BWD, IO, FIT, KG>
       <<<(unsigned)((long long)prm.B * prm.NRB * prm.NCB), kThreads, smem, st>>>(prm);
