@@ -387,7 +387,7 @@ def oracle_fit(ctrl0, w, T, lr, iters):
     return np.array(losses), grads, c
 
 
-@pytest.mark.parametrize("n_s,iters", [(128, 60), (512, 25)])
+@pytest.mark.parametrize("n_s,iters", [(128, 60), (512, 100)])  # config 3: first 100 iterations
 def test_fit_step_trajectory(n_s, iters):
     truth, init = wl.config3_fit(n_s=n_s)
     T64 = oracle.surface_fwd(truth.ctrl, truth.U, truth.V, truth.u, truth.v, 3, 3)
