@@ -125,17 +125,8 @@ __global__ void __launch_bounds__(kThreads) nurbs_derivs_kernel(const Params prm
       }
     }
     __syncthreads();
-    for (int i = 0; i < cn; ++i) {
-      const int target = su_s[i] - P;
-      while (lo < target) {  // uniform: slide the window by one control row
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-          tw[k] = tw[k + 1];
-          tvw[k] = tvw[k + 1];
-        }
-        ++lo;
-        Trow2(lo + P, tw[P], tvw[P]);
-      }
+    // one row: S', S'_u, S'_v from the window (packed FFMA2), Eq.7 quotient rule, normal, stores
+    auto row = [&](int i) {
       float4 Sp = f4(0.f), Su = f4(0.f), Sv = f4(0.f);
 #pragma unroll
       for (int k = 0; k <= P; ++k) {
@@ -169,6 +160,30 @@ __global__ void __launch_bounds__(kThreads) nurbs_derivs_kernel(const Params prm
           normals[o + 1] = ny * inv;
           normals[o + 2] = nz * inv;
         }
+      }
+    };
+    auto advance = [&](int target) {
+      while (lo < target) {  // uniform: slide the window by one control row
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          tw[k] = tw[k + 1];
+          tvw[k] = tvw[k + 1];
+        }
+        ++lo;
+        Trow2(lo + P, tw[P], tvw[P]);
+      }
+    };
+    constexpr int RU = 8;  // rows per unrolled run when the window does not move
+    int i = 0;
+    while (i < cn) {
+      advance(su_s[i] - P);
+      if (i + RU <= cn && su_s[i + RU - 1] - P == lo) {
+#pragma unroll
+        for (int r = 0; r < RU; ++r) row(i + r);
+        i += RU;
+      } else {
+        row(i);
+        ++i;
       }
     }
   }
