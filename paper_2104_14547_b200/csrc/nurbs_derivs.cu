@@ -12,6 +12,10 @@
 
 #include "nurbs_device.cuh"
 
+#ifndef NB_DERIV_RU
+#define NB_DERIV_RU 8
+#endif
+
 namespace nb {
 
 // N and N' of the p+1 non-zero functions at span s: N' from the degree p-1 functions
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) nurbs_derivs_kernel(const Params prm
         Trow2(lo + P, tw[P], tvw[P]);
       }
     };
-    constexpr int RU = 8;  // rows per unrolled run when the window does not move
+    constexpr int RU = NB_DERIV_RU;  // rows per unrolled run when the window does not move
     int i = 0;
     while (i < cn) {
       advance(su_s[i] - P);

@@ -6,6 +6,8 @@ VARIANTS = {
     "base": [],
     "rowcopies": ["-DNB_EXP_ROWCOPIES"],
     "t8192": ["-DNB_TARGET_CTAS=8192"],
+    "dru4": ["-DNB_DERIV_RU=4"],
+    "dru16": ["-DNB_DERIV_RU=16"],
     "xvec": ["--extra-device-vectorization"],
     "expopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "t1184": ["-DNB_TARGET_CTAS=1184"],
