@@ -203,7 +203,10 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
 // 1 TMA bulk copies (one per stage when rows are contiguous, else one per row), 2 2-D TMA
 // tensor copies (two boxes per stage; rows need not be contiguous).
 template <int P, int Q, bool BWD, int IO, bool FIT, bool KG>
-__global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : kMinBlocks_F)
+#ifndef NB_MINB_F_TMAP
+#define NB_MINB_F_TMAP 6  // the tensor-map forward is shared-memory-limited to 6 CTAs: use their registers
+#endif
+__global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_MINB_F_TMAP : kMinBlocks_F))
     nurbs_grid_kernel(const __grid_constant__ Params prm) {
   constexpr bool BULK = IO >= 1;
   static_assert(!FIT || BWD, "the fitting step is a backward variant");

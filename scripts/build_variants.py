@@ -8,6 +8,8 @@ VARIANTS = {
     "t8192": ["-DNB_TARGET_CTAS=8192"],
     "dru4": ["-DNB_DERIV_RU=4"],
     "dru16": ["-DNB_DERIV_RU=16"],
+    "ftm6": ["-DNB_MINB_F_TMAP=6"],
+    "ftm5": ["-DNB_MINB_F_TMAP=5"],
     "xvec": ["--extra-device-vectorization"],
     "expopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "t1184": ["-DNB_TARGET_CTAS=1184"],
