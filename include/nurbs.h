@@ -46,7 +46,10 @@
  *   Shape checks always run on the host. Data checks (knots, parameters, weights live on
  *   the device) run in nurbs_validate / nurbs_tables, and inside fwd/bwd when the
  *   environment variable NURBS_CHECK=1 (then those calls synchronize). Unchecked, invalid
- *   data never causes out-of-bounds access: spans are clamped into [p, n-1].
+ *   data (out-of-domain or unsorted samples, decreasing knots) gives wrong values but never
+ *   out-of-bounds access: spans are clamped into [p, n-1] and into each tile's band, and the
+ *   rolling row window only moves forward. Tables must come from nurbs_tables for the same
+ *   shape (checked mode verifies their header; the Python binding checks their shape).
  *   nurbs_last_error_detail() returns a thread-local message naming the offending value.
  */
 #ifndef NURBS_B200_H
@@ -72,7 +75,8 @@ enum {
     NURBS_E_UNSORTED = 6,     /* u or v not non-decreasing                                */
     NURBS_E_CUDA = 7,         /* a CUDA runtime error (detail names it)                   */
     NURBS_E_WORKSPACE = 8,    /* workspace NULL or smaller than nurbs_*_workspace_bytes   */
-    NURBS_E_TABLES = 9        /* tables given with knots_batched = 1, or mismatched header */
+    NURBS_E_TABLES = 9        /* tables given with knots_batched = 1, or (checked mode) a table
+                                 header that does not match the call's shape */
 };
 
 typedef struct {
@@ -112,6 +116,14 @@ int    nurbs_surface_bwd(const nurbs_shape* shape, const float* ctrl,
                          float* grad_ctrl, float* grad_U, float* grad_V,
                          void* workspace, size_t ws_bytes, void* stream);
 size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* shape);
+
+/* Diagnostic: the launch plan the grid kernels use for `shape` (a pure function of the
+ * shape, which is what makes results bitwise repeatable). Writes plan[0..5] = K (knot spans
+ * of u per row block), row blocks, column blocks (128 samples of v each), control rows per
+ * band, 1 if one tile per surface (no cross-tile reduction) else 0, CTAs per launch
+ * (saturated at INT32_MAX). Curves (m = 1, q = 0) are planned as one row of the grid.
+ * Host only; returns NURBS_E_ARG for NULL or an invalid shape. */
+int    nurbs_grid_plan(const nurbs_shape* shape, int32_t plan[6]);
 
 /* ---------------------------------------------------------------------------------------
  * Parametric derivatives (Eq.7 P:196-209 and its v analogue) and unit normals
@@ -203,6 +215,19 @@ int    nurbs_curve_bwd(const nurbs_shape* shape, const float* ctrl, const float*
                        float* grad_ctrl, float* grad_U,
                        void* workspace, size_t ws_bytes, void* stream);
 size_t nurbs_curve_bwd_workspace_bytes(const nurbs_shape* shape);
+
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU point sharding. When one surface's parameter
+ * rows are sharded over ranks, each rank's backward returns a PARTIAL gradient (the Eq.8/9
+ * sums of P:215/P:222 over its own points); the full gradient is their sum. After an
+ * all-gather of the partials, nurbs_sum_partials adds them in ascending part order:
+ *   out[k] = ((parts[0][k] + parts[1][k]) + parts[2][k]) + ... ,  k < n
+ * so the result is bitwise repeatable for a fixed number of parts (an NCCL all-reduce's
+ * summation order depends on its algorithm and protocol). parts: DEVICE [n_parts][n] fp32;
+ * out: DEVICE [n] fp32 (may alias parts[0]); asynchronous on `stream`. NURBS_E_ARG for
+ * n_parts < 1, n < 0 or NULL pointers (n = 0 is a no-op).
+ * --------------------------------------------------------------------------------------- */
+int    nurbs_sum_partials(const float* parts, int32_t n_parts, int64_t n, float* out, void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * Checked mode. nurbs_validate checks every data precondition (knots non-decreasing and

@@ -73,6 +73,30 @@ class OracleError(RuntimeError):
     pass
 
 
+def cores() -> int:
+    """Host threads the oracle may use (the process's CPU affinity, else os.cpu_count())."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:  # pragma: no cover
+        return max(1, os.cpu_count() or 1)
+
+
+def pmap(fn, items, threads: int | None = None) -> list:
+    """[fn(*it) for it in items] on a pool of host threads, results in item order.
+
+    The C oracle is called through ctypes, which releases the GIL, so the calls run in
+    parallel (SURVEY.md §8(c) "Threading": threads over surfaces or u-row blocks; callers
+    combine partial results in item order, so the result does not depend on the thread
+    count)."""
+    from concurrent.futures import ThreadPoolExecutor
+    items = list(items)
+    threads = threads or cores()
+    if threads <= 1 or len(items) <= 1:
+        return [fn(*it) for it in items]
+    with ThreadPoolExecutor(max_workers=min(threads, len(items))) as ex:
+        return list(ex.map(lambda it: fn(*it), items))
+
+
 def _d(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
@@ -152,8 +176,9 @@ def surface_fwd(ctrl, U, V, u, v, p: int, q: int, knots_batched: bool = False) -
 
 
 def surface_bwd(ctrl, U, V, u, v, gout, p: int, q: int, knots_batched: bool = False,
-                form: str = "H") -> np.ndarray:
-    """Gradient [B][n][m][4] = dL/d(x,y,z,w). form='H' homogeneous, 'E' literal Eq.8/9."""
+                form: str = "E") -> np.ndarray:
+    """Gradient [B][n][m][4] = dL/d(x,y,z,w). form='E' (default) is the literal Eq.8 /
+    Eq.9 sum; form='H' the homogeneous rewrite, pinned equal to it."""
     ctrl, U, V, u, v, dims = _surf_args(ctrl, U, V, u, v, p, q, knots_batched)
     B, n, m = dims[:3]
     g = _d(gout)

@@ -21,6 +21,8 @@ from .api import (  # noqa: F401
     surface_shape,
     curve_shape,
     bwd_workspace_bytes,
+    grid_plan,
+    nurbs_sum_partials,
     fit_workspace_bytes,
     nurbs_surface_fit_step,
     SurfaceFitter,

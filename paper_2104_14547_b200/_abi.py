@@ -26,7 +26,7 @@ EXPORTS = ["nurbs_tables_bytes", "nurbs_tables", "nurbs_surface_fwd", "nurbs_sur
            "nurbs_last_error_detail", "nurbs_abi_version", "nurbs_surface_points_fwd",
            "nurbs_surface_points_bwd", "nurbs_surface_points_bwd_workspace_bytes", "nurbs_validate_points",
            "nurbs_surface_bwd_knots", "nurbs_surface_bwd_knots_workspace_bytes", "nurbs_curve_bwd_knots",
-           "nurbs_curve_bwd_knots_workspace_bytes"]
+           "nurbs_curve_bwd_knots_workspace_bytes", "nurbs_grid_plan", "nurbs_sum_partials"]
 
 
 class nurbs_shape(ctypes.Structure):
@@ -78,6 +78,8 @@ def load() -> ctypes.CDLL:
         "nurbs_strerror": ([I], ctypes.c_char_p),
         "nurbs_last_error_detail": ([], ctypes.c_char_p),
         "nurbs_abi_version": ([], I),
+        "nurbs_grid_plan": ([sh, ctypes.POINTER(ctypes.c_int32)], I),
+        "nurbs_sum_partials": ([P, ctypes.c_int32, ctypes.c_int64, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -34,6 +34,45 @@ def _ptr(x):
     raise TypeError(f"cannot pass {type(x)} as a device pointer")
 
 
+def _sizes(sh: nurbs_shape) -> dict:
+    """Element counts every tensor argument must have for shape `sh` (include/nurbs.h)."""
+    kb = sh.B if sh.knots_batched else 1
+    curve = sh.m == 1 and sh.q == 0
+    return {"ctrl": sh.B * sh.n * sh.m * 4, "U": kb * (sh.n + sh.p + 1),
+            "V": None if curve else kb * (sh.m + sh.q + 1), "u": sh.n_u, "v": None if curve else sh.n_v,
+            "pts": sh.B * sh.n_u * sh.n_v * 3}
+
+
+def _expect(sh: nurbs_shape, **named):
+    """Raise ValueError unless every tensor argument is float32 with exactly the element count
+    the shape implies (a wrong size would make the kernels read or write out of bounds; a
+    float64 tensor would be reinterpreted). Raw device addresses (ints) are the caller's
+    responsibility, as in C. `kind` of each keyword: ctrl, U, V, u, v or pts."""
+    sz = _sizes(sh)
+    for key, t in named.items():
+        if not isinstance(t, torch.Tensor):
+            continue
+        kind = key.split("_")[0]
+        if t.dtype != _F32:
+            raise ValueError(f"{key}: expected float32, got {t.dtype}")
+        want = sz[kind]
+        if want is not None and t.numel() != want:
+            raise ValueError(f"{key}: expected {want} elements for shape (B={sh.B}, n={sh.n}, m={sh.m}, "
+                             f"p={sh.p}, q={sh.q}, n_u={sh.n_u}, n_v={sh.n_v}, "
+                             f"knots_batched={sh.knots_batched}), got {t.numel()} {tuple(t.shape)}")
+
+
+def _expect_tables(sh: nurbs_shape, tables):
+    """Tables are built for one shape: refuse them for another (their offsets would be wrong)."""
+    if isinstance(tables, Tables):
+        a, b = tables.shape, sh
+        fa = tuple(getattr(a, f) for f, _ in nurbs_shape._fields_ if f != "B")
+        fb = tuple(getattr(b, f) for f, _ in nurbs_shape._fields_ if f != "B")
+        if fa != fb or (a.knots_batched and a.B != b.B):
+            raise ValueError(f"tables were built for (n, m, p, q, n_u, n_v, knots_batched) = {fa}, "
+                             f"the call has {fb}")
+
+
 def _stream(stream):
     if stream is None:
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -66,19 +105,32 @@ def bwd_workspace_bytes(sh: nurbs_shape) -> int:
     return int(f(ctypes.byref(sh)))
 
 
+def grid_plan(sh: nurbs_shape) -> dict:
+    """The grid kernels' launch plan for `sh` (nurbs_grid_plan; host only)."""
+    out = (ctypes.c_int32 * 6)()
+    check(load().nurbs_grid_plan(ctypes.byref(sh), out), "nurbs_grid_plan")
+    return dict(zip(("K", "row_blocks", "col_blocks", "band_rows", "direct", "ctas"), list(out)))
+
+
 # ----------------------------------------------------------------------------- C ABI mirror
 def nurbs_tables(sh, U, V, u, v, tables, stream=None):
+    _expect(sh, U=U, V=V, u=u, v=v)
     check(load().nurbs_tables(ctypes.byref(sh), _ptr(U), _ptr(V), _ptr(u), _ptr(v), _ptr(tables),
                               _stream(stream)), "nurbs_tables")
 
 
 def nurbs_surface_fwd(sh, ctrl, U, V, u, v, tables, out, stream=None):
+    _expect(sh, ctrl=ctrl, U=U, V=V, u=u, v=v, pts_out=out)
+    _expect_tables(sh, tables)
     check(load().nurbs_surface_fwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
                                    _ptr(tables), _ptr(out), _stream(stream)), "nurbs_surface_fwd")
 
 
 def nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, grad_U, grad_V,
                       workspace, ws_bytes, stream=None):
+    _expect(sh, ctrl=ctrl, U=U, V=V, u=u, v=v, pts_grad_out=grad_out, ctrl_grad=grad_ctrl, U_grad=grad_U,
+            V_grad=grad_V)
+    _expect_tables(sh, tables)
     check(load().nurbs_surface_bwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
                                    _ptr(tables), _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U),
                                    _ptr(grad_V), _ptr(workspace), ctypes.c_size_t(ws_bytes),
@@ -86,11 +138,15 @@ def nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, grad_U,
 
 
 def nurbs_curve_fwd(sh, ctrl, U, u, tables, out, stream=None):
+    _expect(sh, ctrl=ctrl, U=U, u=u, pts_out=out)
+    _expect_tables(sh, tables)
     check(load().nurbs_curve_fwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(u), _ptr(tables), _ptr(out),
                                  _stream(stream)), "nurbs_curve_fwd")
 
 
 def nurbs_curve_bwd(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspace, ws_bytes, stream=None):
+    _expect(sh, ctrl=ctrl, U=U, u=u, pts_grad_out=grad_out, ctrl_grad=grad_ctrl, U_grad=grad_U)
+    _expect_tables(sh, tables)
     check(load().nurbs_curve_bwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(u), _ptr(tables),
                                  _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U), _ptr(workspace),
                                  ctypes.c_size_t(ws_bytes), _stream(stream)), "nurbs_curve_bwd")
@@ -98,6 +154,8 @@ def nurbs_curve_bwd(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspa
 
 def nurbs_surface_fit_step(sh, ctrl, U, V, u, v, tables, target, lr, grad_ctrl, loss, workspace, ws_bytes,
                            stream=None):
+    _expect(sh, ctrl=ctrl, U=U, V=V, u=u, v=v, pts_target=target, ctrl_grad=grad_ctrl)
+    _expect_tables(sh, tables)
     check(load().nurbs_surface_fit_step(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
                                         _ptr(tables), _ptr(target), ctypes.c_float(lr), _ptr(grad_ctrl),
                                         _ptr(loss), _ptr(workspace), ctypes.c_size_t(ws_bytes), _stream(stream)),
@@ -105,6 +163,7 @@ def nurbs_surface_fit_step(sh, ctrl, U, V, u, v, tables, target, lr, grad_ctrl, 
 
 
 def nurbs_surface_derivs(sh, ctrl, U, V, u, v, out, out_u, out_v, normals, stream=None):
+    _expect(sh, ctrl=ctrl, U=U, V=V, u=u, v=v, pts_out=out, pts_u=out_u, pts_v=out_v, pts_normals=normals)
     check(load().nurbs_surface_derivs(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v), _ptr(out),
                                       _ptr(out_u), _ptr(out_v), _ptr(normals), _stream(stream)),
           "nurbs_surface_derivs")
@@ -126,7 +185,17 @@ def fit_workspace_bytes(sh: nurbs_shape) -> int:
     return int(load().nurbs_surface_fit_workspace_bytes(ctypes.byref(sh)))
 
 
+def nurbs_sum_partials(parts, out, stream=None):
+    """out[k] = sum over r (ascending) of parts[r][k] — the fixed-order sum of the per-rank
+    partial gradients of a point-sharded backward (include/nurbs.h). parts: [R][n] float32."""
+    if parts.dtype != _F32 or out.dtype != _F32 or parts.dim() != 2 or out.numel() != parts.shape[1]:
+        raise ValueError(f"parts must be float32 [R][n] and out float32 [n]; got {tuple(parts.shape)}, {tuple(out.shape)}")
+    check(load().nurbs_sum_partials(_ptr(parts), parts.shape[0], out.numel(), _ptr(out), _stream(stream)),
+          "nurbs_sum_partials")
+
+
 def nurbs_validate(sh, ctrl, U, V, u, v, stream=None):
+    _expect(sh, ctrl=ctrl, U=U, V=V, u=u, v=v)
     check(load().nurbs_validate(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
                                 _stream(stream)), "nurbs_validate")
 
@@ -140,6 +209,9 @@ def knots_workspace_bytes(sh: nurbs_shape) -> int:
 
 def nurbs_surface_bwd_knots(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes,
                             stream=None):
+    _expect(sh, ctrl=ctrl, U=U, V=V, u=u, v=v, pts_grad_out=grad_out, ctrl_grad=grad_ctrl, U_grad=grad_U,
+            V_grad=grad_V)
+    _expect_tables(sh, tables)
     check(load().nurbs_surface_bwd_knots(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(u), _ptr(v),
                                          _ptr(tables), _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U), _ptr(grad_V),
                                          _ptr(workspace), ctypes.c_size_t(ws_bytes), _stream(stream)),
@@ -147,6 +219,8 @@ def nurbs_surface_bwd_knots(sh, ctrl, U, V, u, v, tables, grad_out, grad_ctrl, g
 
 
 def nurbs_curve_bwd_knots(sh, ctrl, U, u, tables, grad_out, grad_ctrl, grad_U, workspace, ws_bytes, stream=None):
+    _expect(sh, ctrl=ctrl, U=U, u=u, pts_grad_out=grad_out, ctrl_grad=grad_ctrl, U_grad=grad_U)
+    _expect_tables(sh, tables)
     check(load().nurbs_curve_bwd_knots(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(u), _ptr(tables), _ptr(grad_out),
                                        _ptr(grad_ctrl), _ptr(grad_U), _ptr(workspace), ctypes.c_size_t(ws_bytes),
                                        _stream(stream)), "nurbs_curve_bwd_knots")
@@ -186,13 +260,22 @@ def points_workspace_bytes(sh: nurbs_shape) -> int:
     return int(load().nurbs_surface_points_bwd_workspace_bytes(ctypes.byref(sh)))
 
 
+def _expect_points(sh, uv=None, **named):
+    _expect(sh, **named)
+    if isinstance(uv, torch.Tensor) and (uv.dtype != _F32 or uv.numel() != sh.B * sh.n_u * 2):
+        raise ValueError(f"uv: expected float32 [B={sh.B}][N={sh.n_u}][2], got {uv.dtype} {tuple(uv.shape)}")
+
+
 def nurbs_surface_points_fwd(sh, ctrl, U, V, uv, out, stream=None):
+    _expect_points(sh, uv, ctrl=ctrl, U=U, V=V, pts_out=out)
     check(load().nurbs_surface_points_fwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(uv), _ptr(out),
                                           _stream(stream)), "nurbs_surface_points_fwd")
 
 
 def nurbs_surface_points_bwd(sh, ctrl, U, V, uv, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes,
                              stream=None):
+    _expect_points(sh, uv, ctrl=ctrl, U=U, V=V, pts_grad_out=grad_out, ctrl_grad=grad_ctrl, U_grad=grad_U,
+                   V_grad=grad_V)
     check(load().nurbs_surface_points_bwd(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(uv),
                                           _ptr(grad_out), _ptr(grad_ctrl), _ptr(grad_U), _ptr(grad_V),
                                           _ptr(workspace), ctypes.c_size_t(ws_bytes), _stream(stream)),
@@ -200,6 +283,7 @@ def nurbs_surface_points_bwd(sh, ctrl, U, V, uv, grad_out, grad_ctrl, grad_U, gr
 
 
 def nurbs_validate_points(sh, ctrl, U, V, uv, stream=None):
+    _expect_points(sh, uv, ctrl=ctrl, U=U, V=V)
     check(load().nurbs_validate_points(ctypes.byref(sh), _ptr(ctrl), _ptr(U), _ptr(V), _ptr(uv), _stream(stream)),
           "nurbs_validate_points")
 

@@ -9,8 +9,6 @@ from __future__ import annotations
 
 import glob
 import os
-import shutil
-import tempfile
 import subprocess
 import sys
 
@@ -41,26 +39,47 @@ def deps():
     return glob.glob(os.path.join(CSRC, "*")) + [os.path.join(ROOT, "include", "nurbs.h")]
 
 
+OBJ_CACHE = os.path.join(HERE, "build_obj")  # per-unit objects keyed by a hash of their inputs
+
+
+def _unit_key(src: str, flags) -> str:
+    """Hash of a unit's source, every header under csrc/ + include/nurbs.h, and its flags."""
+    import hashlib
+    h = hashlib.sha256()
+    for path in [src] + sorted(p for p in deps() if not p.endswith(".cu")):
+        with open(path, "rb") as f:
+            h.update(os.path.relpath(path, ROOT).encode() + b"\0" + f.read())
+    h.update(" ".join(flags).encode())
+    return h.hexdigest()[:24]
+
+
 def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()) -> str:
+    """Compile every unit for sm_100a (units whose inputs are unchanged come from the object
+    cache) and link libnurbs_b200.so. Rebuilds only when a source is newer than the library."""
     LIB_ = lib
     stale = force or not os.path.exists(LIB_) or any(os.path.getmtime(d) > os.path.getmtime(LIB_) for d in deps())
     if not stale:
         return LIB_
-    OBJ = tempfile.mkdtemp(prefix="nurbs_b200_obj_")
-    procs = []
+    os.makedirs(OBJ_CACHE, exist_ok=True)
+    procs, objs = [], []
     for name, src, extra in units():
-        obj = os.path.join(OBJ, name + ".o")
-        cmd = [NVCC] + FLAGS + list(defines) + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+        flags = FLAGS + list(defines) + extra
+        obj = os.path.join(OBJ_CACHE, f"{name}-{_unit_key(src, flags)}.o")
+        objs.append(obj)
+        if os.path.exists(obj) and not force:
+            continue
+        cmd = [NVCC] + flags + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj + ".tmp"]
         procs.append((name, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
-    objs, failed = [], False
+    failed = False
     for name, obj, pr in procs:
         out, _ = pr.communicate()
         if pr.returncode != 0:
             failed = True
             sys.stderr.write(f"--- {name}\n{out}")
-        elif verbose:
-            sys.stderr.write(out)
-        objs.append(obj)
+        else:
+            os.replace(obj + ".tmp", obj)
+            if verbose:
+                sys.stderr.write(out)
     if failed:
         raise RuntimeError("nvcc failed building libnurbs_b200.so")
     res = subprocess.run([NVCC] + ARCH + ["-shared", "-o", LIB_ + ".tmp"] + objs, capture_output=True, text=True)
@@ -68,7 +87,14 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
     os.replace(LIB_ + ".tmp", LIB_)
-    shutil.rmtree(OBJ, ignore_errors=True)
+    # keep the cache small: drop objects of units that are no longer current
+    keep = {os.path.basename(o) for o in objs}
+    for f in os.listdir(OBJ_CACHE):
+        if f.endswith(".o") and f not in keep and not defines:
+            try:
+                os.remove(os.path.join(OBJ_CACHE, f))
+            except OSError:
+                pass
     return LIB_
 
 

@@ -99,10 +99,25 @@ Geo curve_geo(const nurbs_shape* sh, const float* U, const float* u) {
   return g;
 }
 
-void attach_tables(Geo& g, const void* tables) {
-  if (!tables) return;
+// Point the directions at a caller's tables. In checked mode (NURBS_CHECK=1) the device
+// header written by nurbs_tables is read back (synchronizes) and must match this call's shape:
+// tables built for another n, degree or sample count would be read at wrong offsets.
+int attach_tables(Geo& g, const void* tables, cudaStream_t st) {
+  if (!tables) return NURBS_OK;
   const nb::TabLayout L = nb::tab_layout(g.P > 0 ? g.r.ns : 0, g.r.p, g.c.ns, g.c.p);
   const unsigned char* t = static_cast<const unsigned char*>(tables);
+  if (check_mode()) {
+    int h[10] = {};
+    cudaError_t e = cudaMemcpyAsync(h, tables, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "tables header read");
+    const int want[10] = {(int)nb::kTabMagic, 1, g.P > 0 ? g.r.n : h[2], g.P > 0 ? g.r.p : h[3], g.P > 0 ? g.r.ns : 0,
+                          L.np_r, g.c.n, g.c.p, g.c.ns, L.np_c};
+    for (int k = 0; k < 10; ++k)
+      if (h[k] != want[k])
+        return fail(NURBS_E_TABLES, "tables header field %d is %d, this call needs %d (tables built for another shape)",
+                    k, h[k], want[k]);
+  }
   if (g.P > 0) {
     g.r.tspan = reinterpret_cast<const int*>(t + L.off_span_r);
     g.r.tN = reinterpret_cast<const float*>(t + L.off_N_r);
@@ -111,6 +126,7 @@ void attach_tables(Geo& g, const void* tables) {
   g.c.tspan = reinterpret_cast<const int*>(t + L.off_span_c);
   g.c.tN = reinterpret_cast<const float*>(t + L.off_N_c);
   g.c.tnp = L.np_c;
+  return NURBS_OK;
 }
 
 // ---- 2-D TMA descriptor of a streamed [rows][n_v][3] fp32 tensor (out, dL/dS or the fit
@@ -449,7 +465,7 @@ int nurbs_surface_bwd_knots(const nurbs_shape* sh, const float* ctrl, const floa
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Geo g = surface_geo(sh, U, V, u, v);
   if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
-  attach_tables(g, tables);
+  if ((st = attach_tables(g, tables, s))) return st;
   return launch_knots(g, ctrl, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes, s);
 }
 
@@ -467,7 +483,7 @@ int nurbs_curve_bwd_knots(const nurbs_shape* sh, const float* ctrl, const float*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Geo g = curve_geo(sh, U, u);
   if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
-  attach_tables(g, tables);
+  if ((st = attach_tables(g, tables, s))) return st;
   return launch_knots(g, ctrl, grad_out, grad_ctrl, nullptr, grad_U, workspace, ws_bytes, s);
 }
 
@@ -553,6 +569,17 @@ int nurbs_surface_points_bwd(const nurbs_shape* sh, const float* ctrl, const flo
 
 int nurbs_abi_version(void) { return NURBS_ABI_VERSION; }
 
+int nurbs_sum_partials(const float* parts, int32_t n_parts, int64_t n, float* out, void* stream) {
+  g_detail.clear();
+  if (n_parts < 1 || n < 0) return fail(NURBS_E_ARG, "n_parts = %d, n = %lld", (int)n_parts, (long long)n);
+  if (n == 0) return NURBS_OK;
+  if (!parts || !out) return fail(NURBS_E_ARG, "NULL pointer");
+  if (((n & 3) == 0) && (!aligned16(parts) || !aligned16(out)))
+    return fail(NURBS_E_ARG, "parts and out must be 16-byte aligned");
+  cudaError_t e = nb::launch_sum_partials(parts, n_parts, (long long)n, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? NURBS_OK : cuda_fail(e, "sum_partials kernel launch");
+}
+
 const char* nurbs_strerror(int status) {
   switch (status) {
     case NURBS_OK: return "ok";
@@ -616,6 +643,19 @@ size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* sh) {
   return nb::make_plan(sh->B, sh->n, sh->p, sh->n_u, sh->m, sh->n_v).ws_bytes;
 }
 
+int nurbs_grid_plan(const nurbs_shape* sh, int32_t plan[6]) {
+  g_detail.clear();
+  if (!plan) return fail(NURBS_E_ARG, "plan is NULL");
+  const bool curve = sh && sh->m == 1 && sh->q == 0;
+  int st = curve ? check_curve_shape(sh) : check_surface_shape(sh);
+  if (st) return st;
+  Geo g = curve ? curve_geo(sh, nullptr, nullptr) : surface_geo(sh, nullptr, nullptr, nullptr, nullptr);
+  const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns);
+  plan[0] = pl.K; plan[1] = pl.NRB; plan[2] = pl.NCB; plan[3] = pl.T_rows; plan[4] = pl.direct;
+  plan[5] = pl.grid > 0x7fffffffLL ? 0x7fffffff : (int32_t)pl.grid;
+  return NURBS_OK;
+}
+
 size_t nurbs_surface_fit_workspace_bytes(const nurbs_shape* sh) {
   if (!sh || sh->B <= 0) return 0;
   return nb::make_plan(sh->B, sh->n, sh->p, sh->n_u, sh->m, sh->n_v).fit_ws_bytes;
@@ -635,7 +675,7 @@ int nurbs_surface_fit_step(const nurbs_shape* sh, float* ctrl, const float* U, c
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Geo g = surface_geo(sh, U, V, u, v);
   if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
-  attach_tables(g, tables);
+  if ((st = attach_tables(g, tables, s))) return st;
   return launch_fit(g, ctrl, target, lr, grad_ctrl, loss, workspace, ws_bytes, s);
 }
 
@@ -694,7 +734,7 @@ int nurbs_surface_fwd(const nurbs_shape* sh, const float* ctrl, const float* U, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Geo g = surface_geo(sh, U, V, u, v);
   if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
-  attach_tables(g, tables);
+  if ((st = attach_tables(g, tables, s))) return st;
   return launch(g, false, ctrl, out, nullptr, nullptr, nullptr, nullptr, nullptr, 0, s);
 }
 
@@ -717,7 +757,7 @@ int nurbs_surface_bwd(const nurbs_shape* sh, const float* ctrl, const float* U, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Geo g = surface_geo(sh, U, V, u, v);
   if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
-  attach_tables(g, tables);
+  if ((st = attach_tables(g, tables, s))) return st;
   return launch(g, true, ctrl, nullptr, grad_out, grad_ctrl, grad_U, grad_V, workspace, ws_bytes, s);
 }
 
@@ -733,7 +773,7 @@ int nurbs_curve_fwd(const nurbs_shape* sh, const float* ctrl, const float* U, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Geo g = curve_geo(sh, U, u);
   if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
-  attach_tables(g, tables);
+  if ((st = attach_tables(g, tables, s))) return st;
   return launch(g, false, ctrl, out, nullptr, nullptr, nullptr, nullptr, nullptr, 0, s);
 }
 
@@ -756,7 +796,7 @@ int nurbs_curve_bwd(const nurbs_shape* sh, const float* ctrl, const float* U, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Geo g = curve_geo(sh, U, u);
   if (check_mode() && (st = validate_geo(g, ctrl, s))) return st;
-  attach_tables(g, tables);
+  if ((st = attach_tables(g, tables, s))) return st;
   return launch(g, true, ctrl, nullptr, grad_out, grad_ctrl, nullptr, grad_U, workspace, ws_bytes, s);
 }
 

@@ -191,7 +191,10 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
           if (a.sv_s[mid] <= j + Q) bend = mid + 1; else bh2 = mid;
         }
         const float4* Hr = a.Hring + ((i - a.band_lo) & (kHRing - 1)) * kCB;
-        for (int bb = blo; bb < bend; ++bb) a4 = fma4v(a.Nv_s[bb * NQ + (j - a.sv_s[bb] + Q)], Hr[bb], a4);
+        for (int bb = blo; bb < bend; ++bb) {
+          const int h = j - a.sv_s[bb] + Q;  // in [0, Q] for sorted v; guarded for unsorted v
+          if (h >= 0 && h <= Q) a4 = fma4v(a.Nv_s[bb * NQ + h], Hr[bb], a4);
+        }
       }
       store_dq(i, j, a4);
     }
@@ -318,8 +321,10 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
       int sp = C.tspan ? __ldg(C.tspan + bb) : d_find_span(Vk, m, Q, __ldg(C.s + bb));
       return min(max(sp, Q), m - 1);
     };
+    // spans of the first and last column (sorted v); max() keeps the band non-empty and
+    // in bounds when v is not sorted (unchecked mode: wrong values, never out of bounds)
     const int jlo = cspan(B0) - Q;
-    const int ncol = cspan(B0 + cols - 1) - jlo + 1;
+    const int ncol = max(cspan(B0 + cols - 1), jlo + Q) - jlo + 1;
     const int use_smem = ncol <= prm.CBW;
     misc[0] = jlo;
     misc[1] = use_smem;
@@ -427,16 +432,19 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
     d_basis<Q>(Vk, sv, vb, Q, nv);
   }
   sv = min(max(sv, Q), m - 1);
-  if constexpr (BWD) {
-    sv_s[tid] = sv;
-#pragma unroll
-    for (int h = 0; h < NQ; ++h) Nv_s[tid * NQ + h] = h <= Q ? nv[h <= Q ? h : 0] : 0.f;
-  }
 
   // ---- F1 on demand: T(i) = sum_h Nv[h] Q[i][sv - q + h]  (P:140 homogeneous points)
   mbar_wait(band_bar, 0);
   const int jlo = misc[0];
   const bool band_in_smem = misc[1] != 0;
+  // the block's spans lie in [jlo + Q, jlo + ncol - 1] when v is sorted; clamping keeps the
+  // band reads and B2's column indices in bounds for unsorted v too (memory safety only)
+  sv = min(max(sv, jlo + Q), jlo + misc[2] - 1);
+  if constexpr (BWD) {
+    sv_s[tid] = sv;
+#pragma unroll
+    for (int h = 0; h < NQ; ++h) Nv_s[tid * NQ + h] = h <= Q ? nv[h <= Q ? h : 0] : 0.f;
+  }
   const float4* cb0 = cband + (sv - Q - jlo) - (size_t)band_lo * prm.CBW;  // smem band, row 0
   const float4* cg0 = ctrl_s + (sv - Q);                                     // global, row 0
 
@@ -576,8 +584,10 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   // One row of the walk: advance the window to the row's span if it changed (uniform across
   // the CTA, rare: once per knot span), then F2 (+ B1). ci = row index in the smem tables.
   auto row_step = [&](int ci, float* io, auto flush, bool chg) {
+    // the window only moves forward: a row whose span is below the window's (unsorted u,
+    // unchecked mode) is evaluated with the current window — wrong values, never out of bounds
     const int target = chg ? su_s[ci] - P : lo;
-    if (target != lo) {
+    if (target > lo) {
       do {  // row lo is complete
         if constexpr (BWD) flush(lo, acc[0]);
 #pragma unroll

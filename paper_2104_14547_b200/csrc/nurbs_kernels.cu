@@ -213,6 +213,42 @@ cudaError_t launch_tables(const Dir& r, const Dir& c, void* tables, const TabLay
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------ ordered partial sum
+// out[k] = sum over parts r = 0, 1, ... (ascending) of parts[r][k] (multi-GPU point sharding:
+// the rank partials of the backward, after an all-gather). float4 when n % 4 == 0.
+__global__ void __launch_bounds__(256) nurbs_sum_partials_kernel(const float* __restrict__ parts, int np, long long n,
+                                                                 float* out) {
+  const long long gsz = (long long)gridDim.x * blockDim.x;
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((n & 3) == 0) {
+    const long long n4 = n >> 2;
+    const float4* p4 = reinterpret_cast<const float4*>(parts);
+    for (long long i = i0; i < n4; i += gsz) {
+      float4 a = __ldg(p4 + i);
+      for (int r = 1; r < np; ++r) {
+        const float4 b = __ldg(p4 + (long long)r * n4 + i);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      reinterpret_cast<float4*>(out)[i] = a;
+    }
+  } else {
+    for (long long i = i0; i < n; i += gsz) {
+      float a = __ldg(parts + i);
+      for (int r = 1; r < np; ++r) a += __ldg(parts + (long long)r * n + i);
+      out[i] = a;
+    }
+  }
+}
+
+cudaError_t launch_sum_partials(const float* parts, int np, long long n, float* out, cudaStream_t st) {
+  const long long work = (n & 3) == 0 ? n / 4 : n;
+  long long blocks = (work + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  nurbs_sum_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(parts, np, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_validate(int B, const Dir& r, const Dir& c, int check_rows, const float4* ctrl,
                             long long n_ctrl, unsigned long long* status, cudaStream_t st) {
   nurbs_validate_kernel<<<148 * 4, 256, 0, st>>>(B, r, c, check_rows, ctrl, n_ctrl, status);

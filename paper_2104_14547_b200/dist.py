@@ -44,6 +44,46 @@ class GradBuffer:
         return self.flat.numel() * 4
 
 
-def allreduce_grads(buf: GradBuffer, group=None) -> None:
-    """Sum the per-rank partial gradients (fp32, NCCL over NVLink / NVSwitch on GPUs)."""
-    dist.all_reduce(buf.flat, op=dist.ReduceOp.SUM, group=group)
+# NCCL settings that fix the all-reduce's summation order for a given world size and
+# topology (one algorithm, one protocol); set before the process group is created. With
+# `ordered=True` the order is fixed by construction instead (all-gather + rank-order sum).
+NCCL_DETERMINISTIC_ENV = {"NCCL_ALGO": "Ring", "NCCL_PROTO": "Simple"}
+
+
+def pin_nccl_order() -> dict:
+    """Set NCCL_ALGO / NCCL_PROTO (unless the caller already did); returns what is in effect."""
+    import os
+    for k, v in NCCL_DETERMINISTIC_ENV.items():
+        os.environ.setdefault(k, v)
+    return {k: os.environ[k] for k in NCCL_DETERMINISTIC_ENV}
+
+
+class OrderedReducer:
+    """All-gather of the per-rank partials into [world][N], then ONE fixed-order sum
+    (ascending rank) in the library's nurbs_sum_partials kernel: bitwise repeatable for a
+    given world size whatever NCCL's algorithm. Costs an all-gather of world x N floats (8 MB
+    for config 5 at G = 8) instead of an all-reduce of N."""
+
+    def __init__(self, buf: GradBuffer, group=None, sum_fn=None):
+        self.world = dist.get_world_size(group)
+        self.group = group
+        self.gathered = torch.empty(self.world * buf.flat.numel(), dtype=buf.flat.dtype, device=buf.flat.device)
+        if sum_fn is None:
+            if not buf.flat.is_cuda:
+                raise RuntimeError("OrderedReducer sums on the GPU (nurbs_sum_partials); pass sum_fn for host tensors")
+            from .api import nurbs_sum_partials
+            sum_fn = nurbs_sum_partials
+        self.sum_fn = sum_fn
+
+    def __call__(self, buf: GradBuffer) -> None:
+        dist.all_gather_into_tensor(self.gathered, buf.flat, group=self.group)
+        self.sum_fn(self.gathered.view(self.world, -1), buf.flat)
+
+
+def allreduce_grads(buf: GradBuffer, group=None, reducer: "OrderedReducer | None" = None) -> None:
+    """Sum the per-rank partial gradients: one NCCL all-reduce over NVLink / NVSwitch (order
+    fixed by pin_nccl_order), or, with an OrderedReducer, all-gather + rank-order sum."""
+    if reducer is not None:
+        reducer(buf)
+    else:
+        dist.all_reduce(buf.flat, op=dist.ReduceOp.SUM, group=group)

@@ -26,3 +26,23 @@ def cuda_available() -> bool:
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+# ---- parity error log: every GPU parity check records its worst normwise error here; with
+# NB_PARITY_LOG=<path> the session writes them as JSON lines (test, case, kind, error)
+_ERRS: list = []
+
+
+def record(case, kind, err):
+    test = os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0]
+    _ERRS.append({"test": test, "case": case, "kind": kind, "err": float(err)})
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("NB_PARITY_LOG")
+    if path and _ERRS:
+        import json
+        os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+        with open(path, "w") as f:
+            for e in _ERRS:
+                f.write(json.dumps(e) + "\n")

@@ -77,14 +77,59 @@ def test_shape_errors_need_no_gpu(lib):
     assert lib.nurbs_surface_fwd(ctypes.byref(batched), 16, 16, 16, 16, 16, 32, 16, P) == 9  # tables+batched
 
 
-def test_plan_is_bounded():
-    """Row-block bands never exceed the kRMax = 16 smem rows; plans cover every span."""
+def test_plan_is_bounded(lib):
+    """The library's own plan (nurbs_grid_plan): row-block bands never exceed the kRMax = 16
+    staged control rows, the row blocks cover every knot span, the column blocks every
+    sample, one tile per surface means no workspace, and the plan is a function of the shape
+    alone (asked twice, same answer)."""
     import math
-    for (B, n, p, n_u, m, n_v) in [(4096, 16, 3, 128, 16, 128), (1, 256, 3, 8192, 256, 8192), (1, 8, 3, 64, 8, 64),
-                                   (1, 32, 3, 512, 32, 512), (7, 40, 5, 9, 11, 300), (1, 6, 3, 100, 6, 100)]:
+    from paper_2104_14547_b200 import _abi, api
+    for (B, n, p, n_u, m, n_v) in [(4096, 16, 3, 128, 16, 128), (512, 16, 3, 128, 16, 128), (1, 256, 3, 8192, 256, 8192),
+                                   (1, 256, 3, 1024, 256, 8192), (1, 8, 3, 64, 8, 64), (1, 32, 3, 512, 32, 512),
+                                   (7, 40, 5, 9, 11, 300), (1, 6, 3, 100, 6, 100)]:
+        sh = _abi.nurbs_shape(B, n, m, p, 3 if m > 3 else 1, n_u, n_v, 0)
+        pl = api.grid_plan(sh)
+        assert pl == api.grid_plan(sh)
         spans = n - p
-        K = spans if spans + p <= 16 else 16 - p
-        while K > 1 and B * math.ceil(spans / K) * math.ceil(n_v / 128) < 592:
-            K = (K + 1) // 2
-        assert K + p <= 16 or n <= 16
-        assert math.ceil(spans / K) * K >= spans
+        assert pl["K"] + p <= 16 or n <= 16
+        assert pl["row_blocks"] * pl["K"] >= spans and (pl["row_blocks"] - 1) * pl["K"] < spans
+        assert pl["col_blocks"] == math.ceil(n_v / 128)
+        assert pl["band_rows"] == min(pl["K"] + p, n)
+        assert pl["ctas"] == B * pl["row_blocks"] * pl["col_blocks"]
+        ws = lib.nurbs_surface_bwd_workspace_bytes(ctypes.byref(sh))
+        assert (ws == 0) == bool(pl["direct"]) and pl["direct"] == (pl["ctas"] == B)
+    # config 4 keeps one CTA per surface (no reduction); config 5 is tiled
+    assert api.grid_plan(_abi.nurbs_shape(4096, 16, 16, 3, 3, 128, 128, 0))["direct"] == 1
+    assert api.grid_plan(_abi.nurbs_shape(1, 256, 256, 3, 3, 8192, 8192, 0))["direct"] == 0
+    curve = api.grid_plan(_abi.nurbs_shape(1, 6, 1, 3, 0, 100, 1, 0))
+    assert curve["row_blocks"] == 1 and curve["col_blocks"] == 1
+    assert lib.nurbs_grid_plan(None, (ctypes.c_int32 * 6)()) == 1
+
+
+def test_binding_rejects_wrong_dtypes_and_sizes():
+    """The Python binding checks dtype and element counts before any pointer reaches the C
+    ABI (a wrong size would read out of bounds, a float64 tensor would be reinterpreted)."""
+    import torch
+    from paper_2104_14547_b200 import _abi, api
+    sh = _abi.nurbs_shape(2, 8, 7, 3, 2, 5, 6, 0)
+    good = dict(ctrl=torch.zeros(2, 8, 7, 4), U=torch.zeros(12), V=torch.zeros(10), u=torch.zeros(5),
+                v=torch.zeros(6), pts_out=torch.zeros(2, 5, 6, 3), ctrl_grad=torch.zeros(2, 8, 7, 4))
+    api._expect(sh, **good)
+    for key, bad in [("ctrl", torch.zeros(2, 8, 7, 4, dtype=torch.float64)), ("U", torch.zeros(11)),
+                     ("V", torch.zeros(11)), ("u", torch.zeros(6)), ("pts_out", torch.zeros(2, 5, 6, 4)),
+                     ("ctrl_grad", torch.zeros(1, 8, 7, 4))]:
+        with pytest.raises(ValueError):
+            api._expect(sh, **{**good, key: bad})
+    kb = _abi.nurbs_shape(2, 8, 7, 3, 2, 5, 6, 1)  # batched knots: [B][n+p+1]
+    api._expect(kb, U=torch.zeros(2, 12), V=torch.zeros(2, 10))
+    with pytest.raises(ValueError):
+        api._expect(kb, U=torch.zeros(12))
+    with pytest.raises(ValueError):   # uv of paired points
+        api._expect_points(_abi.nurbs_shape(2, 8, 7, 3, 2, 9, 1, 0), torch.zeros(2, 8, 2))
+    # tables built for one shape are refused for another
+    t = api.Tables(_abi.nurbs_shape(4, 8, 7, 3, 2, 5, 6, 0), torch.zeros(16, dtype=torch.uint8))
+    api._expect_tables(_abi.nurbs_shape(9, 8, 7, 3, 2, 5, 6, 0), t)        # another batch size is fine
+    with pytest.raises(ValueError):
+        api._expect_tables(_abi.nurbs_shape(4, 8, 7, 3, 2, 5, 7, 0), t)    # another n_v is not
+    with pytest.raises(ValueError):
+        api._expect_tables(_abi.nurbs_shape(4, 9, 7, 3, 2, 5, 6, 0), t)

@@ -1,7 +1,9 @@
 """Multi-process (world_size 2, gloo, CPU) coverage of the N>1 host logic of dist.py:
 u-row sharding of one surface (config 5's partition), the flat gradient buffer the backward
-writes in place, and the single all-reduce that combines the partial gradients. The per-rank
-partials come from the fp64 oracle on that rank's rows (the CUDA path is covered by -m gpu)."""
+writes in place, the single all-reduce (or the all-gather + rank-order sum) that combines the
+partial gradients, and batch sharding of a surface batch (config 4's partition: no
+collective on the data path). The per-rank results come from the fp64 oracle on that rank's
+share (the CUDA path is covered by -m gpu)."""
 import os
 import socket
 
@@ -24,7 +26,15 @@ def free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _rank_order_sum(parts, out):
+    """host stand-in for nurbs_sum_partials (test only): ascending rank order"""
+    acc = parts[0].clone()
+    for r in range(1, parts.shape[0]):
+        acc += parts[r]
+    out.copy_(acc)
+
+
+def _worker(rank, world, port, q, ordered=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -36,7 +46,8 @@ def _worker(rank, world, port, q):
         buf.grad_ctrl.copy_(torch.from_numpy(part.astype(np.float32)))
         buf.grad_U.fill_(0.0)   # the library zero-fills knot gradients
         buf.grad_V.fill_(0.0)
-        nbd.allreduce_grads(buf)
+        red = nbd.OrderedReducer(buf, sum_fn=_rank_order_sum) if ordered else None
+        nbd.allreduce_grads(buf, reducer=red)
         if rank == 0:
             full = oracle.surface_bwd(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q)
             err = float(np.max(np.abs(buf.grad_ctrl.numpy() - full)) / np.max(np.abs(full)))
@@ -67,10 +78,53 @@ def test_gradbuffer_views_share_storage():
 
 
 @pytest.mark.timeout(180)
-def test_row_sharded_backward_allreduce_gloo():
+@pytest.mark.parametrize("ordered", [False, True])
+def test_row_sharded_backward_allreduce_gloo(ordered):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    mp.spawn(_worker, args=(2, free_port(), q), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, free_port(), q, ordered), nprocs=2, join=True)
     err, gU, gV, nbytes = q.get(timeout=60)
     assert err <= 1e-6          # fp32 buffer of fp64 partials, summed in one all-reduce
     assert gU == 0.0 and gV == 0.0
+
+
+def _batch_worker(rank, world, port, q):
+    """Config 4's partition: rank r owns surfaces shard_range(B, world, r) of ONE global batch
+    and computes them with no collective; the gather below is only the test's check."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = wl.surfaces("batch", B=5, n=9, m=8, p=3, q=2, n_u=11, n_v=13, seed=23)   # odd B: ragged shards
+        g = w.grad_out(6)
+        b0, b1 = nbd.shard_range(w.B, world, rank)
+        out = oracle.surface_fwd(w.ctrl[b0:b1], w.U, w.V, w.u, w.v, w.p, w.q)
+        grad = oracle.surface_bwd(w.ctrl[b0:b1], w.U, w.V, w.u, w.v, g[b0:b1], w.p, w.q)
+        counts = [None] * world
+        dist.all_gather_object(counts, (b0, b1, out, grad))
+        if rank == 0:
+            assert [c[0] for c in counts] == [0, 3] and [c[1] for c in counts] == [3, 5]
+            full_out = np.concatenate([c[2] for c in counts])
+            full_grad = np.concatenate([c[3] for c in counts])
+            ref_out = oracle.surface_fwd(w.ctrl, w.U, w.V, w.u, w.v, w.p, w.q)
+            ref_grad = oracle.surface_bwd(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q)
+            q.put((full_out.shape[0], float(np.abs(full_out - ref_out).max()), float(np.abs(full_grad - ref_grad).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_batch_sharded_surfaces_gloo():
+    """Strong batch sharding: the ranks' shards tile the ONE global batch (no surface twice,
+    none missing) and, surfaces being independent (Alg.1), the shard results are
+    exactly the unsharded ones."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_batch_worker, args=(2, free_port(), q), nprocs=2, join=True)
+    B, e_out, e_grad = q.get(timeout=60)
+    assert B == 5 and e_out == 0.0 and e_grad == 0.0
+
+
+def test_pin_nccl_order_keeps_caller_settings(monkeypatch):
+    monkeypatch.delenv("NCCL_ALGO", raising=False)
+    monkeypatch.setenv("NCCL_PROTO", "LL128")
+    assert nbd.pin_nccl_order() == {"NCCL_ALGO": "Ring", "NCCL_PROTO": "LL128"}
