@@ -911,7 +911,10 @@ def run_grid(args, rank, world, local):
     gb = nbd.GradBuffer.alloc(B, n, m, U.numel(), V.numel(), dev)
     ws_bytes = nb.bwd_workspace_bytes(sh)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-    plan = nb.grid_plan(sh)
+    try:
+        plan = nb.grid_plan(sh)
+    except AttributeError:      # an older library under NURBS_B200_LIB_EXPERIMENT (A/B timing)
+        plan = None
     reducer = nbd.OrderedReducer(gb) if (world > 1 and args.config == 5 and args.ordered_reduce) else None
     launches_per_step = 2 + (1 if ws_bytes > 0 else 0) + (1 if reducer is not None else 0)
     points = B * n_u * n_v                      # this rank's points per step

@@ -43,11 +43,13 @@ def _sizes(sh: nurbs_shape) -> dict:
             "pts": sh.B * sh.n_u * sh.n_v * 3}
 
 
-def _expect(sh: nurbs_shape, **named):
-    """Raise ValueError unless every tensor argument is float32 with exactly the element count
-    the shape implies (a wrong size would make the kernels read or write out of bounds; a
-    float64 tensor would be reinterpreted). Raw device addresses (ints) are the caller's
-    responsibility, as in C. `kind` of each keyword: ctrl, U, V, u, v or pts."""
+def _expect(sh: nurbs_shape, exact: bool = False, **named):
+    """Raise ValueError unless every tensor argument is float32 and holds the element count
+    the shape implies: at least that many in the C-ABI mirrors (a smaller buffer would be read
+    or written out of bounds; a larger one, e.g. a reused slot, is only partly used), exactly
+    that many in the convenience wrappers. A float64 tensor would be reinterpreted, so dtype
+    is always checked. Raw device addresses (ints) are the caller's responsibility, as in C.
+    The keyword's prefix names its kind: ctrl, U, V, u, v or pts."""
     sz = _sizes(sh)
     for key, t in named.items():
         if not isinstance(t, torch.Tensor):
@@ -56,7 +58,7 @@ def _expect(sh: nurbs_shape, **named):
         if t.dtype != _F32:
             raise ValueError(f"{key}: expected float32, got {t.dtype}")
         want = sz[kind]
-        if want is not None and t.numel() != want:
+        if want is not None and (t.numel() != want if exact else t.numel() < want):
             raise ValueError(f"{key}: expected {want} elements for shape (B={sh.B}, n={sh.n}, m={sh.m}, "
                              f"p={sh.p}, q={sh.q}, n_u={sh.n_u}, n_v={sh.n_v}, "
                              f"knots_batched={sh.knots_batched}), got {t.numel()} {tuple(t.shape)}")
@@ -260,9 +262,10 @@ def points_workspace_bytes(sh: nurbs_shape) -> int:
     return int(load().nurbs_surface_points_bwd_workspace_bytes(ctypes.byref(sh)))
 
 
-def _expect_points(sh, uv=None, **named):
-    _expect(sh, **named)
-    if isinstance(uv, torch.Tensor) and (uv.dtype != _F32 or uv.numel() != sh.B * sh.n_u * 2):
+def _expect_points(sh, uv=None, exact: bool = False, **named):
+    _expect(sh, exact, **named)
+    if isinstance(uv, torch.Tensor) and (uv.dtype != _F32 or (uv.numel() != sh.B * sh.n_u * 2 if exact
+                                                              else uv.numel() < sh.B * sh.n_u * 2)):
         raise ValueError(f"uv: expected float32 [B={sh.B}][N={sh.n_u}][2], got {uv.dtype} {tuple(uv.shape)}")
 
 
@@ -291,6 +294,7 @@ def nurbs_validate_points(sh, ctrl, U, V, uv, stream=None):
 def surface_points_fwd(ctrl, U, V, uv, p: int, q: int, out=None, stream=None):
     """S at paired points: out [B][N][3] for uv [B][N][2]."""
     sh = points_shape(ctrl, U, uv, p, q)
+    _expect_points(sh, uv, True, ctrl=ctrl, U=U, V=V, pts_out=out)
     if out is None:
         out = torch.empty((sh.B, sh.n_u, 3), dtype=_F32, device=ctrl.device)
     nurbs_surface_points_fwd(sh, ctrl, U, V, uv, out, stream)
@@ -301,6 +305,7 @@ def surface_points_bwd(ctrl, U, V, uv, grad_out, p: int, q: int, grad_ctrl=None,
                        workspace=None, stream=None):
     """dL/d(x,y,z,w) [B][n][m][4] at paired points (deterministic)."""
     sh = points_shape(ctrl, U, uv, p, q)
+    _expect_points(sh, uv, True, ctrl=ctrl, U=U, V=V, pts_grad_out=grad_out, ctrl_grad=grad_ctrl)
     if grad_ctrl is None:
         grad_ctrl = torch.empty_like(ctrl)
     ws = points_workspace_bytes(sh)
@@ -329,6 +334,7 @@ class Tables:
 # ----------------------------------------------------------------------------- wrappers
 def surface_fwd(ctrl, U, V, u, v, p: int, q: int, tables: Tables | None = None, out=None, stream=None):
     sh = surface_shape(ctrl, U, u, v, p, q)
+    _expect(sh, True, ctrl=ctrl, U=U, V=V, u=u, v=v, pts_out=out)
     if out is None:
         out = torch.empty((sh.B, sh.n_u, sh.n_v, 3), dtype=_F32, device=ctrl.device)
     nurbs_surface_fwd(sh, ctrl, U, V, u, v, tables, out, stream)
@@ -338,6 +344,8 @@ def surface_fwd(ctrl, U, V, u, v, p: int, q: int, tables: Tables | None = None, 
 def surface_bwd(ctrl, U, V, u, v, grad_out, p: int, q: int, tables: Tables | None = None,
                 grad_ctrl=None, grad_U=None, grad_V=None, workspace=None, stream=None):
     sh = surface_shape(ctrl, U, u, v, p, q)
+    _expect(sh, True, ctrl=ctrl, U=U, V=V, u=u, v=v, pts_grad_out=grad_out, ctrl_grad=grad_ctrl, U_grad=grad_U,
+            V_grad=grad_V)
     if grad_ctrl is None:
         grad_ctrl = torch.empty_like(ctrl)
     ws = bwd_workspace_bytes(sh)
@@ -349,6 +357,7 @@ def surface_bwd(ctrl, U, V, u, v, grad_out, p: int, q: int, tables: Tables | Non
 
 def curve_fwd(ctrl, U, u, p: int, tables: Tables | None = None, out=None, stream=None):
     sh = curve_shape(ctrl, U, u, p)
+    _expect(sh, True, ctrl=ctrl, U=U, u=u, pts_out=out)
     if out is None:
         out = torch.empty((sh.B, sh.n_u, 3), dtype=_F32, device=ctrl.device)
     nurbs_curve_fwd(sh, ctrl, U, u, tables, out, stream)
@@ -358,6 +367,7 @@ def curve_fwd(ctrl, U, u, p: int, tables: Tables | None = None, out=None, stream
 def curve_bwd(ctrl, U, u, grad_out, p: int, tables: Tables | None = None, grad_ctrl=None, grad_U=None,
               workspace=None, stream=None):
     sh = curve_shape(ctrl, U, u, p)
+    _expect(sh, True, ctrl=ctrl, U=U, u=u, pts_grad_out=grad_out, ctrl_grad=grad_ctrl, U_grad=grad_U)
     if grad_ctrl is None:
         grad_ctrl = torch.empty_like(ctrl)
     ws = bwd_workspace_bytes(sh)

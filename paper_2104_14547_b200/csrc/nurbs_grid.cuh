@@ -588,6 +588,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
     // unchecked mode) is evaluated with the current window — wrong values, never out of bounds
     const int target = chg ? su_s[ci] - P : lo;
     if (target > lo) {
+#ifndef NB_EXP_UNROLL_ADV
+#pragma unroll 1  // keep the (rare) window advance compact: unrolling it bloats the row loop
+#endif
       do {  // row lo is complete
         if constexpr (BWD) flush(lo, acc[0]);
 #pragma unroll

@@ -4,6 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2104_14547_b200.build import build
 VARIANTS = {
     "base": [],
+    "unrolladv": ["-DNB_EXP_UNROLL_ADV"],
     "rowcopies": ["-DNB_EXP_ROWCOPIES"],
     "t8192": ["-DNB_TARGET_CTAS=8192"],
     "dru4": ["-DNB_DERIV_RU=4"],
@@ -27,5 +28,5 @@ os.makedirs("exp", exist_ok=True)
 sel = sys.argv[1:] or list(VARIANTS)
 for name in sel:
     out = os.path.join("exp", f"lib_{name}.so")
-    build(force=True, lib=out, defines=["-DNB_EXPERIMENT_PQ33"] + VARIANTS[name])
+    build(force=False, lib=out, defines=["-DNB_EXPERIMENT_PQ33"] + VARIANTS[name])
     print(name, os.path.getsize(out))

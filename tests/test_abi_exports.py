@@ -114,18 +114,23 @@ def test_binding_rejects_wrong_dtypes_and_sizes():
     sh = _abi.nurbs_shape(2, 8, 7, 3, 2, 5, 6, 0)
     good = dict(ctrl=torch.zeros(2, 8, 7, 4), U=torch.zeros(12), V=torch.zeros(10), u=torch.zeros(5),
                 v=torch.zeros(6), pts_out=torch.zeros(2, 5, 6, 3), ctrl_grad=torch.zeros(2, 8, 7, 4))
-    api._expect(sh, **good)
+    api._expect(sh, True, **good)
+    api._expect(sh, ctrl_grad=torch.zeros(3, 8, 7, 4))       # a larger buffer passes the C-ABI mirrors
+    with pytest.raises(ValueError):
+        api._expect(sh, True, ctrl_grad=torch.zeros(3, 8, 7, 4))  # ... but not the convenience wrappers
     for key, bad in [("ctrl", torch.zeros(2, 8, 7, 4, dtype=torch.float64)), ("U", torch.zeros(11)),
                      ("V", torch.zeros(11)), ("u", torch.zeros(6)), ("pts_out", torch.zeros(2, 5, 6, 4)),
                      ("ctrl_grad", torch.zeros(1, 8, 7, 4))]:
         with pytest.raises(ValueError):
-            api._expect(sh, **{**good, key: bad})
+            api._expect(sh, True, **{**good, key: bad})
     kb = _abi.nurbs_shape(2, 8, 7, 3, 2, 5, 6, 1)  # batched knots: [B][n+p+1]
-    api._expect(kb, U=torch.zeros(2, 12), V=torch.zeros(2, 10))
+    api._expect(kb, True, U=torch.zeros(2, 12), V=torch.zeros(2, 10))
     with pytest.raises(ValueError):
         api._expect(kb, U=torch.zeros(12))
     with pytest.raises(ValueError):   # uv of paired points
         api._expect_points(_abi.nurbs_shape(2, 8, 7, 3, 2, 9, 1, 0), torch.zeros(2, 8, 2))
+    with pytest.raises(ValueError):   # float64 is never reinterpreted
+        api._expect(sh, ctrl=torch.zeros(4, 8, 7, 4, dtype=torch.float64))
     # tables built for one shape are refused for another
     t = api.Tables(_abi.nurbs_shape(4, 8, 7, 3, 2, 5, 6, 0), torch.zeros(16, dtype=torch.uint8))
     api._expect_tables(_abi.nurbs_shape(9, 8, 7, 3, 2, 5, 6, 0), t)        # another batch size is fine
