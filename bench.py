@@ -55,6 +55,8 @@ def parse(argv=None):
     ap.add_argument("--shard-of", type=int, default=0, help="one GPU: time rank 0's shard of a G-way split")
     ap.add_argument("--weak", action="store_true", help="config 4: every rank its own 4096 surfaces")
     ap.add_argument("--ordered-reduce", action="store_true", help="config 5: all-gather + rank-order sum")
+    ap.add_argument("--tc", action="store_true",
+                    help="time the tcgen05 (3xTF32) backward instead of the SIMT backward where it applies")
     ap.add_argument("--iters", type=int, default=1000, help="config 3: SGD iterations per fit (one step)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="oracle cpu_baseline budget per leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -878,13 +880,23 @@ def run_grid(args, rank, world, local):
     from paper_2104_14547_b200 import dist as nbd
     import workloads as wl
 
+    # NB_BENCH_SHARE_GPU=1 (plumbing check only): N ranks on the visible GPUs round-robin, with a
+    # gloo group (NCCL refuses two ranks on one GPU); timings are then not scaling numbers
+    share = os.environ.get("NB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         if args.config == 5 and not args.ordered_reduce:
             nbd.pin_nccl_order()
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     assert args.warmup >= 3, "timing rules need >= 3 warm-up steps"
+    if args.tc:
+        nb.path_flags(tc=True).__enter__()
 
     hbm_peak, peak_kind = load_peaks()
     stream = torch.cuda.current_stream()
@@ -959,7 +971,7 @@ def run_grid(args, rank, world, local):
     fwd_ms = sum(ev[3 * k].elapsed_time(ev[3 * k + 1]) for k in range(K)) / K
     bwd_ms = sum(ev[3 * k + 1].elapsed_time(ev[3 * k + 2]) for k in range(K)) / K
     red_ms = sum(ev[3 * k + 2].elapsed_time(ev[3 * k + 3]) for k in range(K)) / K
-    t = torch.tensor([total_ms, fwd_ms, bwd_ms, red_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, fwd_ms, bwd_ms, red_ms], dtype=torch.float64, device="cpu" if share else dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, fwd_ms, bwd_ms, red_ms = t.tolist()
@@ -976,7 +988,9 @@ def run_grid(args, rank, world, local):
     fwd_bytes = points * 12 + ctrl_bytes + tab_bytes
     bwd_bytes = points * 12 + 2 * ctrl_bytes + tab_bytes + (U.numel() + V.numel()) * 4
     if bwd_ms >= fwd_ms:
-        kname, kbytes, kms = "nurbs_grid_kernel<3,3,true,IO,false,false> (bwd)", bwd_bytes, bwd_ms
+        kname = ("nb::tc::nurbs_bwd_tc_kernel<3,3,16,IO> (bwd)" if args.tc
+                 else "nurbs_grid_kernel<3,3,true,IO,false,false> (bwd)")
+        kbytes, kms = bwd_bytes, bwd_ms
     else:
         kname, kbytes, kms = "nurbs_grid_kernel<3,3,false,IO,false,false> (fwd)", fwd_bytes, fwd_ms
     achieved = kbytes / (kms * 1e-3) / 1e9
@@ -993,6 +1007,24 @@ def run_grid(args, rank, world, local):
                 "step": {"ms": fwd_ms + bwd_ms, "bytes": step_bytes,
                          "gbs": step_bytes / ((fwd_ms + bwd_ms) * 1e-3) / 1e9,
                          "frac": step_bytes / ((fwd_ms + bwd_ms) * 1e-3) / 1e9 / hbm_peak}}
+
+    # ---------------- the tcgen05 backward (3xTF32, nurbs_bwd_tc.cu) timed beside the SIMT one
+    tc_line = None
+    if not args.tc and world == 1 and args.config == 4:
+        with nb.path_flags(tc=True):
+            for _ in range(3):
+                bwd()
+            torch.cuda.synchronize()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(min(K, 50)):
+                bwd()
+            t1.record(stream)
+            torch.cuda.synchronize()
+        tc_ms = t0.elapsed_time(t1) / min(K, 50)
+        tc_line = {"kernel": "nb::tc::nurbs_bwd_tc_kernel<3,3,16,IO> (tcgen05.mma kind::tf32, 3xTF32)", "ms": tc_ms,
+                   "gbs": bwd_bytes / (tc_ms * 1e-3) / 1e9, "frac": bwd_bytes / (tc_ms * 1e-3) / 1e9 / hbm_peak,
+                   "note": "opt-in path (NURBS_TC=1 / path_flags(tc=True)); the SIMT backward is the default"}
 
     # ---------------- e2e: host buffers through the public API, copies inside the timed region
     e2e = None
@@ -1017,7 +1049,7 @@ def run_grid(args, rank, world, local):
             pipe.fwd_bwd(h_ctrl, h_gout, h_out, h_grad, stream)
         e1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cpu" if share else dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = te.item() / E
@@ -1074,7 +1106,7 @@ def run_grid(args, rank, world, local):
         stream.wait_event(ev_o)  # the last download is inside the timed region
         e1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cpu" if share else dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = te.item() / E
@@ -1113,6 +1145,8 @@ def run_grid(args, rank, world, local):
             "bwd_ms": bwd_ms,
             "allreduce_ms": red_ms if (world > 1 and args.config == 5) else None,
             "allreduce_bytes": gb.nbytes if args.config == 5 else None,
+            "bwd_path": "tcgen05 3xTF32 (--tc)" if args.tc else "SIMT grid kernel",
+            "tc_bwd": tc_line,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

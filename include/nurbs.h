@@ -237,6 +237,16 @@ int    nurbs_sum_partials(const float* parts, int32_t n_parts, int64_t n, float*
 int         nurbs_validate(const nurbs_shape* shape, const float* ctrl, const float* U,
                            const float* V, const float* u, const float* v, void* stream);
 const char* nurbs_strerror(int status);
+
+/* Path selection (process-wide; defaults from the environment variables NURBS_NO_TMA /
+ * NURBS_TC at first use). NURBS_PATH_NO_TMA: stream out / dL/dS with per-thread global
+ * accesses instead of TMA (results bitwise identical). NURBS_PATH_TC: run the surface backward
+ * on the tcgen05 tensor cores (3xTF32) where it applies (p = q = 3, m <= 32);
+ * results equal the SIMT backward's within rounding, not bitwise. Returns the previous flags.
+ * Not for use while other threads launch. */
+#define NURBS_PATH_NO_TMA 1
+#define NURBS_PATH_TC     2
+int         nurbs_set_path_flags(int flags);
 const char* nurbs_last_error_detail(void);
 int         nurbs_abi_version(void);
 

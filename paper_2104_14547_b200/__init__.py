@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     curve_shape,
     bwd_workspace_bytes,
     grid_plan,
+    path_flags,
     nurbs_sum_partials,
     fit_workspace_bytes,
     nurbs_surface_fit_step,

@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NURBS_B200_LIB_EXPERIMENT") or os.path.join(HERE, "libnurbs_b200.so")
 
 NURBS_OK = 0
+NURBS_PATH_NO_TMA, NURBS_PATH_TC = 1, 2
 NURBS_MAX_DEGREE = 5
 STATUS_NAMES = {0: "NURBS_OK", 1: "NURBS_E_ARG", 2: "NURBS_E_UNSUPPORTED", 3: "NURBS_E_KNOTS",
                 4: "NURBS_E_DOMAIN", 5: "NURBS_E_WEIGHT", 6: "NURBS_E_UNSORTED", 7: "NURBS_E_CUDA",
@@ -26,7 +27,7 @@ EXPORTS = ["nurbs_tables_bytes", "nurbs_tables", "nurbs_surface_fwd", "nurbs_sur
            "nurbs_last_error_detail", "nurbs_abi_version", "nurbs_surface_points_fwd",
            "nurbs_surface_points_bwd", "nurbs_surface_points_bwd_workspace_bytes", "nurbs_validate_points",
            "nurbs_surface_bwd_knots", "nurbs_surface_bwd_knots_workspace_bytes", "nurbs_curve_bwd_knots",
-           "nurbs_curve_bwd_knots_workspace_bytes", "nurbs_grid_plan", "nurbs_sum_partials"]
+           "nurbs_curve_bwd_knots_workspace_bytes", "nurbs_grid_plan", "nurbs_sum_partials", "nurbs_set_path_flags"]
 
 
 class nurbs_shape(ctypes.Structure):
@@ -80,6 +81,7 @@ def load() -> ctypes.CDLL:
         "nurbs_abi_version": ([], I),
         "nurbs_grid_plan": ([sh, ctypes.POINTER(ctypes.c_int32)], I),
         "nurbs_sum_partials": ([P, ctypes.c_int32, ctypes.c_int64, P, P], I),
+        "nurbs_set_path_flags": ([I], I),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("NURBS_B200_LIB_EXPERIMENT") and not hasattr(L, name):

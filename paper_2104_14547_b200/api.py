@@ -107,6 +107,23 @@ def bwd_workspace_bytes(sh: nurbs_shape) -> int:
     return int(f(ctypes.byref(sh)))
 
 
+class path_flags:
+    """Context manager selecting kernel paths (nurbs_set_path_flags), e.g.
+    ``with path_flags(no_tma=True): ...`` runs the per-thread IO path and
+    ``with path_flags(tc=True): ...`` the tensor-core backward; restores on exit."""
+
+    def __init__(self, no_tma: bool = False, tc: bool = False):
+        from ._abi import NURBS_PATH_NO_TMA, NURBS_PATH_TC
+        self.flags = (NURBS_PATH_NO_TMA if no_tma else 0) | (NURBS_PATH_TC if tc else 0)
+
+    def __enter__(self):
+        self.prev = load().nurbs_set_path_flags(self.flags)
+        return self
+
+    def __exit__(self, *exc):
+        load().nurbs_set_path_flags(self.prev)
+
+
 def grid_plan(sh: nurbs_shape) -> dict:
     """The grid kernels' launch plan for `sh` (nurbs_grid_plan; host only)."""
     out = (ctypes.c_int32 * 6)()

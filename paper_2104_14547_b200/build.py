@@ -27,7 +27,8 @@ def units():
          ("nurbs_kernels", os.path.join(CSRC, "nurbs_kernels.cu"), []),
          ("nurbs_derivs", os.path.join(CSRC, "nurbs_derivs.cu"), []),
          ("nurbs_points", os.path.join(CSRC, "nurbs_points.cu"), []),
-         ("nurbs_knots", os.path.join(CSRC, "nurbs_knots.cu"), [])]
+         ("nurbs_knots", os.path.join(CSRC, "nurbs_knots.cu"), []),
+         ("nurbs_bwd_tc", os.path.join(CSRC, "nurbs_bwd_tc.cu"), [])]
     for p in range(6):
         u.append((f"nurbs_grid_p{p}", os.path.join(CSRC, "nurbs_grid_p.cu"), [f"-DNB_P={p}"]))
     for p in range(1, 6):

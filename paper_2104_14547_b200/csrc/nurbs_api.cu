@@ -1,6 +1,7 @@
 // nurbs_api.cu — host side of the C ABI declared in include/nurbs.h: shape checks, the
 // launch plan, checked mode, and the kernel launches on the caller's stream.
 // Citations: P:n = reference/PAPER.md line n; R<k> = DESIGN.md §3 reading k.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -49,6 +50,20 @@ bool check_mode() {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Diagnostic switches, read once per process: NURBS_NO_TMA=1 forces the per-thread IO path,
+// NURBS_TC=1 runs the tensor-core backward (nurbs_bwd_tc.cu) where it applies.
+bool env_flag(const char* name) {
+  const char* s = getenv(name);
+  return s && s[0] && s[0] != '0';
+}
+std::atomic<int>& path_flags() {
+  static std::atomic<int> f{(env_flag("NURBS_NO_TMA") ? NURBS_PATH_NO_TMA : 0) |
+                           (env_flag("NURBS_TC") ? NURBS_PATH_TC : 0)};
+  return f;
+}
+bool no_tma() { return (path_flags().load(std::memory_order_relaxed) & NURBS_PATH_NO_TMA) != 0; }
+bool use_tc() { return (path_flags().load(std::memory_order_relaxed) & NURBS_PATH_TC) != 0; }
 
 // Shape rules shared by surfaces and curves (one direction).
 int check_dir(const char* name, int n, int p, int ns) {
@@ -151,6 +166,17 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 void set_io_map(nb::Params& prm, const float* base, long long rows, int nv, int rps) {
   prm.tmap = 0;
   if (!prm.bulk || nv < nb::kBoxCols || (nv == nb::kCB && prm.NCB == 1) || rows <= 0) return;
+  // the descriptor is a pure function of (base, rows, nv, rps): a per-thread cache of recent
+  // encodes keeps the driver call off the per-launch path of repeated calls
+  struct Entry { const float* base; long long rows; int nv, rps; CUtensorMap map; };
+  static thread_local Entry cache[4];
+  static thread_local int next = 0;
+  for (const Entry& c : cache)
+    if (c.base == base && c.rows == rows && c.nv == nv && c.rps == rps) {
+      prm.io_map = c.map;
+      prm.tmap = 1;
+      return;
+    }
   PFN_cuTensorMapEncodeTiled_v12000 fn = tmap_encoder();
   if (!fn) return;
   const cuuint64_t dims[2] = {(cuuint64_t)nv * 3, (cuuint64_t)rows};
@@ -159,8 +185,11 @@ void set_io_map(nb::Params& prm, const float* base, long long rows, int nv, int 
   const cuuint32_t es[2] = {1, 1};
   if (fn(&prm.io_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
     prm.tmap = 1;
+    cache[next] = Entry{base, rows, nv, rps, prm.io_map};
+    next = (next + 1) & 3;
+  }
 }
 
 // Checked mode: validate data on the device and synchronize.
@@ -227,13 +256,15 @@ int launch(const Geo& g, bool bwd, const float* ctrl, float* out, const float* g
   prm.direct = pl.direct;
   const void* io = bwd ? static_cast<const void*>(gout) : static_cast<const void*>(out);
   prm.bulk = (g.c.ns % 4 == 0) && aligned16(io) ? 1 : 0;
-  if (getenv("NURBS_NO_TMA")) prm.bulk = 0;
+  if (no_tma()) prm.bulk = 0;
   if (bwd && !pl.direct) {
     prm.slots = reinterpret_cast<float4*>(ws);
     prm.colband = reinterpret_cast<int2*>(static_cast<unsigned char*>(ws) + pl.slots_bytes);
   }
   set_io_map(prm, bwd ? gout : out, (long long)g.B * g.r.ns, g.c.ns, bwd ? nb::kRPS_B : nb::kRPS_F);
-  cudaError_t e = nb::launch_grid(prm, bwd ? 1 : 0, g.P, g.c.p, st);
+  cudaError_t e = cudaErrorNotSupported;
+  if (bwd && use_tc() && nb::bwd_tc_supported(prm, g.P, g.c.p)) e = nb::launch_bwd_tc(prm, g.P, g.c.p, st);
+  if (e == cudaErrorNotSupported) e = nb::launch_grid(prm, bwd ? 1 : 0, g.P, g.c.p, st);
   if (e != cudaSuccess) return cuda_fail(e, bwd ? "backward kernel launch" : "forward kernel launch");
   if (bwd && !pl.direct) {
     e = nb::launch_reduce(prm, g.P, st);
@@ -270,7 +301,7 @@ int launch_fit(const Geo& g, float* ctrl, const float* target, float lr, float* 
   prm.CBW = g.c.n < nb::kBandCols ? g.c.n : nb::kBandCols;
   prm.direct = pl.direct;
   prm.bulk = (g.c.ns % 4 == 0) && aligned16(target) ? 1 : 0;
-  if (getenv("NURBS_NO_TMA")) prm.bulk = 0;
+  if (no_tma()) prm.bulk = 0;
   unsigned char* w = static_cast<unsigned char*>(ws);
   if (!pl.direct) {
     prm.slots = reinterpret_cast<float4*>(w);
@@ -353,7 +384,7 @@ int launch_knots(const Geo& g, const float* ctrl, const float* gout, float* gctr
   prm.CBW = g.c.n < nb::kBandCols ? g.c.n : nb::kBandCols;
   prm.direct = pl.direct;
   prm.bulk = (g.c.ns % 4 == 0) && aligned16(gout) ? 1 : 0;
-  if (getenv("NURBS_NO_TMA")) prm.bulk = 0;
+  if (no_tma()) prm.bulk = 0;
   if (!pl.direct) {
     prm.slots = reinterpret_cast<float4*>(w);
     prm.colband = reinterpret_cast<int2*>(w + pl.slots_bytes);
@@ -568,6 +599,8 @@ int nurbs_surface_points_bwd(const nurbs_shape* sh, const float* ctrl, const flo
 
 
 int nurbs_abi_version(void) { return NURBS_ABI_VERSION; }
+
+int nurbs_set_path_flags(int flags) { return path_flags().exchange(flags & (NURBS_PATH_NO_TMA | NURBS_PATH_TC)); }
 
 int nurbs_sum_partials(const float* parts, int32_t n_parts, int64_t n, float* out, void* stream) {
   g_detail.clear();

@@ -182,6 +182,9 @@ cudaError_t launch_tables(const Dir& r, const Dir& c, void* tables, const TabLay
 cudaError_t launch_validate(int B, const Dir& r, const Dir& c, int check_rows,
                             const float4* ctrl, long long n_ctrl,
                             unsigned long long* status, cudaStream_t st);
+// tensor-core backward (nurbs_bwd_tc.cu): cudaErrorNotSupported for shapes it does not cover
+bool bwd_tc_supported(const Params& prm, int P, int q);
+cudaError_t launch_bwd_tc(const Params& prm, int P, int q, cudaStream_t st);
 cudaError_t launch_sum_partials(const float* parts, int np, long long n, float* out, cudaStream_t st);
 size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg = false, bool tmap = false);
 

@@ -178,7 +178,7 @@ def test_ragged_columns_and_non_tma_path(n_v):
 
 @pytest.mark.parametrize("n_u,n_v,tables", [(45, 64, False), (13, 196, True), (70, 132, False), (9, 256, False),
                                              (37, 324, True), (200, 68, True)])
-def test_tensor_map_path(n_u, n_v, tables, monkeypatch):
+def test_tensor_map_path(n_u, n_v, tables):
     """n_v % 4 == 0 and rows not contiguous per stage: the 2-D TMA tensor path (two 64-column
     boxes per 8-row stage, per-row fallback for a partial last stage, ragged second box; with
     tables the forward's cp.async row-table prefetch over several 64-row chunks). Against the
@@ -187,21 +187,48 @@ def test_tensor_map_path(n_u, n_v, tables, monkeypatch):
     check_surface(w, tables=tables)
     g = w.grad_out(2)
     a = run_surface(w, g, tables)
-    monkeypatch.setenv("NURBS_NO_TMA", "1")
-    b = run_surface(w, g, tables)
+    with nb.path_flags(no_tma=True):
+        b = run_surface(w, g, tables)
     np.testing.assert_array_equal(a[0], b[0])
     np.testing.assert_array_equal(a[1], b[1])
 
 
 @pytest.mark.parametrize("force_no_tma", [False, True])
-def test_tma_and_direct_paths_agree(force_no_tma, monkeypatch):
+def test_tma_and_direct_paths_agree(force_no_tma):
     w = wl.config4(B=8)
     g = w.grad_out(1)
     a = run_surface(w, g)
-    monkeypatch.setenv("NURBS_NO_TMA", "1")
-    b = run_surface(w, g)
+    with nb.path_flags(no_tma=force_no_tma):
+        b = run_surface(w, g)
     np.testing.assert_array_equal(a[0], b[0])
     np.testing.assert_array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("case", ["cfg2", "cfg4", "m32", "tiled", "ragged", "tmap_tail"])
+def test_tensor_core_backward_matches_simt_and_oracle(case):
+    """The tcgen05 backward (3xTF32 MMAs, nurbs_bwd_tc.cu; NURBS_PATH_TC) covers p = q = 3 and
+    m <= 32; the SIMT grid kernel (the default) is an independent GPU implementation of the same
+    transposed banded product. Both against the oracle at the stated tolerance, against each
+    other within rounding, and the tensor-core path bitwise repeatable, TMA or not."""
+    w = {"cfg2": lambda: wl.config2(),
+         "cfg4": lambda: wl.config4(B=32),
+         "m32": lambda: wl.surfaces("m32", B=3, n=20, m=32, p=3, q=3, n_u=150, n_v=256, seed=12),
+         "tiled": lambda: wl.surfaces("tl", B=2, n=120, m=24, p=3, q=3, n_u=1500, n_v=300, seed=13),
+         "ragged": lambda: wl.surfaces("rg", B=2, n=14, m=11, p=3, q=3, n_u=77, n_v=333, seed=14),
+         "tmap_tail": lambda: wl.surfaces("tt", B=2, n=30, m=9, p=3, q=3, n_u=203, n_v=196, seed=15)}[case]()
+    g = w.grad_out(7)
+    ref = oracle.surface_bwd(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q)
+    with nb.path_flags(tc=True):
+        tc1 = run_surface(w, g)[1]
+        tc2 = run_surface(w, g)[1]
+    with nb.path_flags(tc=True, no_tma=True):
+        tc3 = run_surface(w, g)[1]
+    np.testing.assert_array_equal(tc1, tc2)
+    np.testing.assert_array_equal(tc1, tc3)
+    simt = run_surface(w, g)[1]
+    assert bwd_err(tc1, ref, w.ctrl, f"tc-{case}") <= BWD_TOL
+    assert bwd_err(simt, ref, w.ctrl, f"simt-{case}") <= BWD_TOL
+    assert bwd_err(tc1, simt.astype(np.float64), w.ctrl) <= BWD_TOL
 
 
 def test_sparse_samples_dense_knots():
