@@ -913,15 +913,23 @@ def run_grid(args, rank, world, local):
         B, n, m, n_v = w.B, w.n, w.m, w.n_v
         ctrl_np, u_np = w.ctrl, w.u[lo:hi]
         n_u = hi - lo
+    U_np, r0, r1 = w.U, 0, w.n
+    if args.config == 5 and (hi - lo) < w.n_u:
+        # point sharding: the rank evaluates its u-slab on the sub-net of the control rows its
+        # knot spans touch (local support, dist.row_window): same spans, same knots, same S
+        r0, r1 = nbd.row_window(w.U, w.p, w.n, float(u_np[0]), float(u_np[-1]))
+        ctrl_np, U_np, n = w.ctrl[:, r0:r1], w.U[r0:r1 + w.p + 1], r1 - r0
     T = lambda a: torch.from_numpy(a.copy()).to(dev)  # noqa: E731
-    ctrl, U, V, u, v = T(ctrl_np), T(w.U), T(w.V), T(u_np), T(w.v)
+    ctrl, U, V, u, v = T(ctrl_np), T(U_np), T(w.V), T(u_np), T(w.v)
     sh = nb.nurbs_shape(B, n, m, w.p, w.q, n_u, n_v, 0)
     tables = nb.Tables.build(sh, U, V, u, v)
     out = torch.empty((B, n_u, n_v, 3), dtype=torch.float32, device=dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + lo)              # a function of the unit range: same dL/dS whatever N
     gout = torch.randn((B, n_u, n_v, 3), dtype=torch.float32, device=dev, generator=gen)
-    gb = nbd.GradBuffer.alloc(B, n, m, U.numel(), V.numel(), dev)
+    gb = nbd.GradBuffer.alloc(B, w.n, m, w.U.size, V.numel(), dev)
+    windowed = (r0, r1) != (0, w.n)
+    g_ctrl, g_U = gb.grad_ctrl[:, r0:r1], gb.grad_U[r0:r1 + w.p + 1]   # B = 1: contiguous views
     ws_bytes = nb.bwd_workspace_bytes(sh)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     try:
@@ -936,7 +944,9 @@ def run_grid(args, rank, world, local):
         nb.nurbs_surface_fwd(sh, ctrl, U, V, u, v, tables, out, stream)
 
     def bwd():
-        nb.nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, gout, gb.grad_ctrl, gb.grad_U, gb.grad_V, ws,
+        if windowed:    # rows outside the window are zero in this rank's partial
+            gb.flat.zero_()
+        nb.nurbs_surface_bwd(sh, ctrl, U, V, u, v, tables, gout, g_ctrl, g_U, gb.grad_V, ws,
                              ws_bytes, stream)
 
     def reduce():
@@ -1088,7 +1098,9 @@ def run_grid(args, rank, world, local):
                 h_out.copy_(out, non_blocking=True)
             ev_o.record(s_down)
             stream.wait_event(ev_g)
-            nb.nurbs_surface_bwd(sh, d_ctrl, U, V, u, v, tables, d_gout, gb.grad_ctrl, gb.grad_U, gb.grad_V, ws,
+            if windowed:
+                gb.flat.zero_()
+            nb.nurbs_surface_bwd(sh, d_ctrl, U, V, u, v, tables, d_gout, g_ctrl, g_U, gb.grad_V, ws,
                                  ws_bytes, stream)
             reduce()
             ev_b.record(stream)
@@ -1141,6 +1153,7 @@ def run_grid(args, rank, world, local):
             "config": grid_config(args, world),
             "rank0_units": [lo, hi],
             "plan": plan,
+            "ctrl_rows": [r0, r1],
             "fwd_points_per_s": fwd_value,
             "fwd_ms": fwd_ms,
             "bwd_ms": bwd_ms,

@@ -217,7 +217,7 @@ int validate_geo(const Geo& g, const float* ctrl, cudaStream_t st) {
 
 int launch(const Geo& g, bool bwd, const float* ctrl, float* out, const float* gout, float* gctrl, float* gR,
            float* gC, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns);
+  const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns, !bwd);
   const size_t grad_bytes = (size_t)g.B * g.r.n * g.c.n * 16;
   const int gR_per = g.r.n + g.r.p + 1, gC_per = g.c.n + g.c.p + 1;
   const int gR_items = g.r.kstride ? g.B : 1, gC_items = g.c.kstride ? g.B : 1;

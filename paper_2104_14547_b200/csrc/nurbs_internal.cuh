@@ -7,6 +7,7 @@
 // one sample) and the curve along the columns.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>  // CUtensorMap (the TMA descriptor type; no driver-library link needed)
 #include <cuda_runtime.h>
 
@@ -40,9 +41,6 @@ namespace nb {
 #ifndef NB_MINB_B
 #define NB_MINB_B 4
 #endif
-#ifndef NB_TARGET_CTAS
-#define NB_TARGET_CTAS 2368
-#endif
 
 constexpr int kCB = 128;          // sample columns per CTA block = threads (one column each)
 constexpr int kCompute = 128;     // threads per CTA (4 warps)
@@ -59,8 +57,6 @@ constexpr int kHRing = NB_HRING;         // completed-H rows buffered for B2 (po
 constexpr int kB2Batch = NB_B2BATCH;     // B2 reduces completed rows in batches of this size
 constexpr int kMinBlocks_F = NB_MINB_F;  // __launch_bounds__ min CTAs per SM (register budget)
 constexpr int kMinBlocks_B = NB_MINB_B;
-constexpr int kTargetCTAs = NB_TARGET_CTAS;  // planning target (fixed so the plan, hence the
-                                             // summation order, is a pure function of shape)
 
 // One parametric direction.
 struct Dir {
@@ -143,14 +139,53 @@ struct Plan {
   size_t fit_ws_bytes;      // workspace of the fused fitting step (adds the loss partials)
 };
 
-inline Plan make_plan(int B, int n_r, int P, int ns_r, int n_c, int ns_c) {
+inline int plan_env(const char* name) {  // experiment overrides (NURBS_PLAN_K / _KF); 0 = off
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+// The launch plan: K knot spans of u per row block (halving sequence from the largest K whose
+// band fits kRMax rows), NCB column blocks of kCB samples. A pure function of the shape, so
+// the backward's summation order (hence its bits) is too. Rules fitted to the round-2 plan
+// sweep on one B200 (DESIGN.md §5 "Plan"): per-rank shapes of configs 4 and 5 at G = 1..8.
+//  * backward: one tile per surface (no cross-tile reduce) whenever the surface fits one
+//    tile and there are >= kDirectMinB surfaces; otherwise row blocks of <= kTileRows sample
+//    rows, halved until the grid fills ~0.9 of one wave at kSlotsB CTAs per SM;
+//  * forward (no reduction: only per-tile overhead): the K minimising
+//    ceil(CTAs / slots) * (rows per tile + kTileCost), slots = CTAs resident per SM x SMs.
+constexpr int kSMs = 148;                 // B200
+constexpr int kSlotsB = 4, kSlotsF = 7, kSlotsF_tmap = 6;   // resident CTAs per SM (ptxas / smem)
+constexpr int kDirectMinB = 128;          // direct backward from this many surfaces up
+constexpr int kTileRows = 256;            // backward: sample rows per tile cap (tiled plans)
+constexpr int kTileCost = 40;             // forward: per-tile overhead in sample-row units
+inline Plan make_plan(int B, int n_r, int P, int ns_r, int n_c, int ns_c, bool fwd = false) {
   Plan pl{};
   const int spans = n_r - P;
   pl.NCB = (ns_c + kCB - 1) / kCB;
   int K = spans;
   if (K + P > kRMax) K = kRMax - P;
   if (K < 1) K = 1;
-  while (K > 1 && (long long)B * ((spans + K - 1) / K) * pl.NCB < kTargetCTAs) K = (K + 1) / 2;
+  const int Kmax = K;
+  auto nrb = [&](int k) { return (spans + k - 1) / k; };
+  auto ctas = [&](int k) { return (long long)B * nrb(k) * pl.NCB; };
+  auto half = [](int k) { return (k + 1) / 2; };
+  static const int kforce = plan_env("NURBS_PLAN_K"), kforce_f = plan_env("NURBS_PLAN_KF");
+  const int kf = fwd ? kforce_f : kforce;
+  if (kf > 0) {
+    K = kf < K ? kf : K;
+  } else if (fwd) {
+    const bool tmap = ns_c >= 64 && !(ns_c == kCB && pl.NCB == 1);
+    const long long slots = (long long)kSMs * (tmap ? kSlotsF_tmap : kSlotsF);
+    double best = -1.0;
+    for (int k = Kmax;; k = half(k)) {
+      const double rows = (double)ns_r / nrb(k);
+      const double t = (double)((ctas(k) + slots - 1) / slots) * (rows + kTileCost);
+      if (best < 0.0 || t < best) { best = t; K = k; }
+      if (k == 1) break;
+    }
+  } else if (!(K == spans && pl.NCB == 1 && B >= kDirectMinB)) {
+    while (K > 1 && (long long)ns_r * K > (long long)kTileRows * spans) K = half(K);
+    while (K > 1 && ctas(K) * 10 < 9LL * kSMs * kSlotsB) K = half(K);
+  }
   pl.K = K;
   pl.NRB = (spans + K - 1) / K;
   pl.T_rows = (K + P < n_r) ? (K + P) : n_r;

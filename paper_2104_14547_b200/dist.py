@@ -17,6 +17,28 @@ import torch
 import torch.distributed as dist
 
 
+def row_window(U, p: int, n: int, u_first: float, u_last: float) -> tuple[int, int]:
+    """Control rows [r0, r1) that the samples u in [u_first, u_last] (sorted) can touch.
+
+    Local support (only p+1 basis functions are non-zero at u, those of span s cover
+    control rows s-p..s): a rank that owns the u-rows of a slab needs only the control rows
+    of the knot spans its samples fall in. Passing the sub-net ctrl[:, r0:r1] with the knot
+    slice U[r0 : r1+p+1] (a valid knot vector of n' = r1-r0 control points whose domain
+    [U[r0+p], U[r1]] contains the slab) gives every sample the same span (shifted by r0) and
+    the same knots in A2.2, hence bitwise the same S and the same partial gradient rows
+    (written at row offset r0 of the full gradient). Host logic only: the span of a sample is
+    the largest s with U[s] <= u, clamped to [p, n-1]; the window is widened by one span on
+    each side, so a sample on a knot or at the domain end is covered whatever tie rule
+    FindSpan uses (R3/R4). Returns (r0, r1)."""
+    import numpy as np
+    Uh = np.asarray(U, dtype=np.float32)
+    s = np.searchsorted(Uh, np.array([u_first, u_last], dtype=np.float32), side="right") - 1
+    sa = int(min(max(s[0], p), n - 1))
+    sb = int(min(max(s[1], p), n - 1))
+    sa, sb = max(p, sa - 1), min(n - 1, sb + 1)
+    return sa - p, sb + 1
+
+
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous, balanced split of [0, total) (first `total % world` ranks get one more)."""
     base, extra = divmod(total, world)

@@ -56,6 +56,63 @@ def _worker(rank, world, port, q, ordered=False):
         dist.destroy_process_group()
 
 
+def _window_worker(rank, world, port, q):
+    """Point sharding on the rank's sub-net (dist.row_window): each rank evaluates its u-slab
+    with only the control rows / knots its spans touch, writes its partial gradient at the
+    window's row offset of the full buffer, and ONE all-reduce sums the partials."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = wl.surfaces("win", B=1, n=23, m=7, p=3, q=2, n_u=61, n_v=9, seed=29)
+        g = w.grad_out(8)
+        a0, a1 = nbd.shard_range(w.n_u, world, rank)
+        r0, r1 = nbd.row_window(w.U, w.p, w.n, float(w.u[a0]), float(w.u[a1 - 1]))
+        sub_c, sub_U = w.ctrl[:, r0:r1], w.U[r0:r1 + w.p + 1]
+        out = oracle.surface_fwd(sub_c, sub_U, w.V, w.u[a0:a1], w.v, w.p, w.q)
+        part = oracle.surface_bwd(sub_c, sub_U, w.V, w.u[a0:a1], w.v, g[:, a0:a1], w.p, w.q)
+        buf = nbd.GradBuffer.alloc(w.B, w.n, w.m, len(w.U), len(w.V), "cpu")
+        buf.flat.zero_()
+        buf.grad_ctrl[:, r0:r1].copy_(torch.from_numpy(part.astype(np.float32)))
+        nbd.allreduce_grads(buf)
+        ref_out = oracle.surface_fwd(w.ctrl, w.U, w.V, w.u[a0:a1], w.v, w.p, w.q)
+        outs = [None] * world
+        dist.all_gather_object(outs, (r0, r1, float(np.abs(out - ref_out).max())))
+        if rank == 0:
+            full = oracle.surface_bwd(w.ctrl, w.U, w.V, w.u, w.v, g, w.p, w.q)
+            err = float(np.max(np.abs(buf.grad_ctrl.numpy() - full)) / np.max(np.abs(full)))
+            q.put((outs, err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_row_window_sharding_gloo():
+    """The sub-net of a u-slab gives bitwise the full net's S on the slab (same spans, same
+    knots in A2.2), the windows are proper sub-ranges, and the windowed partial gradients
+    sum (one all-reduce) to the unsharded gradient."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_window_worker, args=(2, free_port(), q), nprocs=2, join=True)
+    outs, err = q.get(timeout=60)
+    assert all(e == 0.0 for _, _, e in outs)
+    assert outs[0][0] == 0 and outs[-1][1] == 23 and all(r1 - r0 < 23 for r0, r1, _ in outs)
+    assert err <= 1e-6
+
+
+def test_row_window_edges():
+    """row_window on clamped knots: samples on interior knots, at 0 and at 1, and a single
+    sample; the window is [s_first-1-p, s_last+2) clamped to [0, n)."""
+    U = wl.clamped_uniform_knots(10, 3)          # spans 3..9, interior knots k/7
+    assert nbd.row_window(U, 3, 10, 0.0, 1.0) == (0, 10)
+    assert nbd.row_window(U, 3, 10, 0.0, 0.0) == (0, 5)       # span 3 (+1) -> rows [0, 5)
+    k3 = float(U[5])                                          # = 2/7: span 5 exactly on the knot
+    assert nbd.row_window(U, 3, 10, k3, k3) == (1, 7)
+    assert nbd.row_window(U, 3, 10, 1.0, 1.0) == (5, 10)      # span 9 (R3) -> [9-1-3, 10)
+    for a, b in [(0.1, 0.2), (0.33, 0.9), (0.5, 0.5)]:
+        r0, r1 = nbd.row_window(U, 3, 10, a, b)
+        assert 0 <= r0 < r1 <= 10 and r1 - r0 >= 4
+
+
 def test_shard_range_partitions():
     for total in (0, 1, 7, 8192, 8191):
         for world in (1, 2, 3, 8):

@@ -480,6 +480,57 @@ def test_config5_full_size():
     check_invariants(grad, g, out, w.ctrl, name="cfg5 full")
 
 
+# --------------------------------------------------------------------------- per-rank shard shapes
+@pytest.mark.parametrize("B", [512, 100])
+def test_config4_rank_shard_plans(B):
+    """Config 4's per-rank batch at G = 8 (B = 512: one tile per surface) and a batch below
+    kDirectMinB (B = 100: tiled plan + cross-tile reduce), in the bench launch configuration
+    (tables), against the fp64 oracle (every surface for B = 100, 32 sampled for B = 512)."""
+    w = wl.config4(B=B)
+    g = w.grad_out(11)
+    pl = nb.grid_plan(nb.nurbs_shape(B, 16, 16, 3, 3, 128, 128, 0))
+    assert pl["direct"] == (1 if B >= 128 else 0)
+    out, grad = run_surface(w, g, tables=True)
+    idx = np.arange(B) if B <= 128 else np.random.default_rng(3).choice(B, 32, replace=False)
+    c = w.ctrl[idx]
+    ro = oracle.surface_fwd(c, w.U, w.V, w.u, w.v, w.p, w.q)
+    rg = oracle.surface_bwd(c, w.U, w.V, w.u, w.v, g[idx], w.p, w.q)
+    ef, eb = fwd_err(out[idx], ro, c, f"cfg4 B={B}"), bwd_err(grad[idx], rg, c, f"cfg4 B={B}")
+    assert ef <= FWD_TOL and eb <= BWD_TOL, (ef, eb)
+
+
+def test_config5_row_window_shards():
+    """Config 5's point sharding as bench.py runs it at G = 8: each rank's u-slab evaluated on
+    its sub-net (dist.row_window). The forward equals the full-net forward of the same rows
+    BITWISE (same spans, same knots, same operations); the windowed partial gradients, placed
+    at their row offsets and summed, match the fp64 oracle's unsharded gradient."""
+    from paper_2104_14547_b200 import dist as nbd
+    w = wl.config5(n_u=2048, n_v=1024)
+    g = w.grad_out(12)
+    ctrl, U, V, u, v = T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v)
+    full_out = nb.surface_fwd(ctrl, U, V, u, v, w.p, w.q).cpu().numpy()
+    total = np.zeros((1, w.n, w.m, 4), dtype=np.float64)
+    G = 8
+    for r in range(G):
+        a0, a1 = nbd.shard_range(w.n_u, G, r)
+        r0, r1 = nbd.row_window(w.U, w.p, w.n, float(w.u[a0]), float(w.u[a1 - 1]))
+        assert r1 - r0 < w.n
+        sc, sU, su = T(w.ctrl[:, r0:r1]), T(w.U[r0:r1 + w.p + 1]), T(w.u[a0:a1])
+        sh = nb.surface_shape(sc, sU, su, v, w.p, w.q)
+        tab = nb.Tables.build(sh, sU, V, su, v)
+        o = nb.surface_fwd(sc, sU, V, su, v, w.p, w.q, tables=tab).cpu().numpy()
+        assert np.array_equal(o, full_out[:, a0:a1]), f"rank {r}: windowed forward differs"
+        gr = nb.surface_bwd(sc, sU, V, su, v, T(g[:, a0:a1]), w.p, w.q, tables=tab).cpu().numpy()
+        total[:, r0:r1] += gr
+    blocks = [(a, min(a + 256, w.n_u)) for a in range(0, w.n_u, 256)]
+    parts = oracle.pmap(lambda a0, a1: oracle.surface_bwd(w.ctrl, w.U, w.V, w.u[a0:a1], w.v, g[:, a0:a1], w.p, w.q),
+                        blocks)
+    ref = np.sum(parts, axis=0)
+    eP, ew = bwd_err_parts(total, ref, w.ctrl)
+    record("cfg5 windows G=8", "dP", eP); record("cfg5 windows G=8", "dw", ew)
+    assert eP <= BWD_TOL and ew <= BWD_TOL, (eP, ew)
+
+
 # --------------------------------------------------------------------------- fused fitting step (NEXT-2)
 def oracle_fit(ctrl0, w, T, lr, iters):
     """fp64 oracle loop of the fitting step: L = mean |S - T|^2, SGD on P and w (Eq.14)."""
