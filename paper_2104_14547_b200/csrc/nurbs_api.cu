@@ -588,6 +588,7 @@ int nurbs_surface_points_bwd(const nurbs_shape* sh, const float* ctrl, const flo
   prm.chunk = pl.chunk_b;
   prm.nchunk = pl.nchunk_b;
   prm.slots = pl.nchunk_b > 1 ? reinterpret_cast<float4*>(workspace) : nullptr;
+  prm.ctrl_smem = pl.ctrl_smem_b;
   e = nb::launch_points(prm, true, sh->p, sh->q, pl.smem_b, s);
   if (e != cudaSuccess) return cuda_fail(e, "paired backward kernel launch");
   if (pl.nchunk_b > 1) {

@@ -24,8 +24,9 @@ PtsPlan pts_plan(int B, int n, int m, int p, int q, int N) {
   while (cf > 64 && pts_fwd_layout(n, m, p, q, (int)cf).bytes > kPtsSmemMax) cf = (cf + 1) / 2;
   pl.chunk_f = (int)cf;
   pl.nchunk_f = N > 0 ? (N + pl.chunk_f - 1) / pl.chunk_f : 0;
-  pl.ctrl_smem = 0;
-  pl.smem_f = pts_fwd_layout(n, m, p, q, pl.chunk_f).bytes;
+  // the homogeneous net in smem when it keeps two CTAs per SM
+  pl.ctrl_smem = pts_fwd_layout(n, m, p, q, pl.chunk_f, true).bytes <= kPtsSmemMax / 2 + 8 * 1024 ? 1 : 0;
+  pl.smem_f = pts_fwd_layout(n, m, p, q, pl.chunk_f, pl.ctrl_smem != 0).bytes;
   // backward: chunks of up to 8192 points (>= ~2 CTAs per SM when the batch is small), as
   // large as the smem budget allows
   long long cb = (pts + 148LL * 2 - 1) / (148LL * 2);
@@ -35,7 +36,8 @@ PtsPlan pts_plan(int B, int n, int m, int p, int q, int N) {
   while (cb > 64 && pts_bwd_layout(n, m, p, q, (int)cb).bytes > kPtsSmemMax) cb = (cb + 1) / 2;
   pl.chunk_b = (int)cb;
   pl.nchunk_b = N > 0 ? (N + pl.chunk_b - 1) / pl.chunk_b : 0;
-  pl.smem_b = pts_bwd_layout(n, m, p, q, pl.chunk_b).bytes;
+  pl.ctrl_smem_b = pts_bwd_layout(n, m, p, q, pl.chunk_b, true).bytes <= kPtsSmemMax / 2 + 8 * 1024 ? 1 : 0;
+  pl.smem_b = pts_bwd_layout(n, m, p, q, pl.chunk_b, pl.ctrl_smem_b != 0).bytes;
   pl.fits_f = ncell <= 65535 && pl.smem_f <= kPtsSmemMax;
   pl.fits_b = ncell <= 65535 && pl.smem_b <= kPtsSmemMax;
   pl.ws_bytes = pl.nchunk_b > 1 ? align_up((size_t)B * pl.nchunk_b * n * m * 16, 256) : 0;

@@ -260,9 +260,9 @@ __device__ __forceinline__ void pts_bucket(const float2* uv, int cnt, int n, int
 // written to HBM coalesced at the end.
 constexpr int kGrpF = 4;
 struct PtsFwdLayout {
-  size_t uv, outs, cstart, hist, cell, sorted, knots, bytes;
+  size_t uv, outs, cstart, hist, cell, sorted, knots, net, bytes;
 };
-__host__ __device__ inline PtsFwdLayout pts_fwd_layout(int n, int m, int p, int q, int chunk) {
+__host__ __device__ inline PtsFwdLayout pts_fwd_layout(int n, int m, int p, int q, int chunk, bool net = false) {
   PtsFwdLayout L;
   const int C = (n - p) * (m - q);
   size_t o = 0;
@@ -275,6 +275,8 @@ __host__ __device__ inline PtsFwdLayout pts_fwd_layout(int n, int m, int p, int 
   L.sorted = o; o += (size_t)chunk * 2;
   o = (o + 15) & ~(size_t)15;
   L.knots = o;  o += (size_t)pts_knots(n, m, p, q).floats * 4;
+  o = (o + 15) & ~(size_t)15;
+  L.net = o;    o += net ? (size_t)n * m * 16 : 0;   // the homogeneous net (ctrl_smem)
   L.bytes = (o + 15) & ~(size_t)15;
   return L;
 }
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_fwd_kernel(PtsPar
   const int n = prm.n, m = prm.m;
   const int Cv = m - Q, C = (n - P) * Cv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const PtsFwdLayout SL = pts_fwd_layout(n, m, P, Q, prm.chunk);
+  const PtsFwdLayout SL = pts_fwd_layout(n, m, P, Q, prm.chunk, prm.ctrl_smem != 0);
   const PtsKnots KL = pts_knots(n, m, P, Q);
   float2* uvs = reinterpret_cast<float2*>(smem + SL.uv);
   float* outs = reinterpret_cast<float*>(smem + SL.outs);
@@ -303,12 +305,15 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_fwd_kernel(PtsPar
   const float2* uv = prm.uv + (size_t)s * prm.N + t0;
   for (int i = tid; i < cnt; i += kPtsThreads) uvs[i] = __ldg(uv + i);
   for (int i = tid; i <= C; i += kPtsThreads) hist[i] = 0;
+  const float4* ctrl_s = prm.ctrl + (size_t)s * n * m;
+  float4* net = reinterpret_cast<float4*>(smem + SL.net);
+  if (prm.ctrl_smem)  // the homogeneous net once per CTA: cells read it with smem broadcasts
+    for (int i = tid; i < n * m; i += kPtsThreads) net[i] = homog(__ldg(ctrl_s + i));
   pts_stage_knots<P, Q>(prm, s, ks);  // ends with __syncthreads
   const float* Us = ks;
   const float* Vs = ks + KL.offV;
   pts_bucket<P, Q>(uvs, cnt, n, m, Us, Vs, hist, cstart, cell, sorted);
 
-  const float4* ctrl_s = prm.ctrl + (size_t)s * n * m;
   const int grp = lane / kGrpF, gl = lane - grp * kGrpF;
   const int G = warp * GPW + grp;
   const int nsteps = (C - warp * GPW + NG - 1) / NG;
@@ -319,10 +324,17 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_fwd_kernel(PtsPar
     if (end <= beg) continue;  // no shuffles below: groups may diverge freely
     const int cu = ce / Cv, cv = ce - cu * Cv;
     float4 Qc[P + 1][Q + 1];   // the cell's homogeneous control points
+    if (prm.ctrl_smem) {
 #pragma unroll
-    for (int r = 0; r <= P; ++r)
+      for (int r = 0; r <= P; ++r)
 #pragma unroll
-      for (int h = 0; h <= Q; ++h) Qc[r][h] = homog(__ldg(ctrl_s + (cu + r) * m + cv + h));
+        for (int h = 0; h <= Q; ++h) Qc[r][h] = net[(cu + r) * m + cv + h];
+    } else {
+#pragma unroll
+      for (int r = 0; r <= P; ++r)
+#pragma unroll
+        for (int h = 0; h <= Q; ++h) Qc[r][h] = homog(__ldg(ctrl_s + (cu + r) * m + cv + h));
+    }
     float ru[RU];  // u record in registers; the v record is read from smem (register budget)
     load_rec<P>(ks + KL.offRU + cu * RU, ru);
     const float* rv = ks + KL.offRV + cv * RV;
@@ -376,9 +388,9 @@ __device__ __forceinline__ void grp_reduce_scatter(float (&acc)[NPAD], int gl) {
 
 // smem carve-up (pts_bwd_smem_bytes mirrors it)
 struct PtsBwdLayout {
-  size_t dq, cstart, hist, cell, sorted, cq, knots, bytes;
+  size_t dq, cstart, hist, cell, sorted, cq, knots, net, bytes;
 };
-__host__ __device__ inline PtsBwdLayout pts_bwd_layout(int n, int m, int p, int q, int chunk) {
+__host__ __device__ inline PtsBwdLayout pts_bwd_layout(int n, int m, int p, int q, int chunk, bool net = false) {
   PtsBwdLayout L;
   const int C = (n - p) * (m - q);
   size_t o = 0;
@@ -390,6 +402,8 @@ __host__ __device__ inline PtsBwdLayout pts_bwd_layout(int n, int m, int p, int 
   L.sorted = o; o += (size_t)chunk * 2;                              // point index by cell
   o = (o + 15) & ~(size_t)15;
   L.knots = o;  o += (size_t)pts_knots(n, m, p, q).floats * 4;
+  o = (o + 15) & ~(size_t)15;
+  L.net = o;    o += net ? (size_t)n * m * 16 : 0;   // the homogeneous net (ctrl_smem)
   L.bytes = (o + 15) & ~(size_t)15;
   return L;
 }
@@ -406,7 +420,7 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_bwd_kernel(PtsPar
   const int n = prm.n, m = prm.m, nm = n * m;
   const int Cv = m - Q, C = (n - P) * Cv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const PtsBwdLayout SL = pts_bwd_layout(n, m, P, Q, prm.chunk);
+  const PtsBwdLayout SL = pts_bwd_layout(n, m, P, Q, prm.chunk, prm.ctrl_smem != 0);
   const PtsKnots KL = pts_knots(n, m, P, Q);
   float4* dqw = reinterpret_cast<float4*>(smem + SL.dq);
   float4* cq = reinterpret_cast<float4*>(smem + SL.cq);
@@ -418,6 +432,9 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_bwd_kernel(PtsPar
 
   for (int i = tid; i < kPtsWarps * nm; i += kPtsThreads) dqw[i] = f4(0.f);
   for (int i = tid; i < kPtsWarps * (C + 1); i += kPtsThreads) hist[i] = 0;
+  float4* net = reinterpret_cast<float4*>(smem + SL.net);
+  if (prm.ctrl_smem)  // the homogeneous net once per CTA
+    for (int i = tid; i < nm; i += kPtsThreads) net[i] = homog(__ldg(prm.ctrl + (size_t)s * nm + i));
   pts_stage_knots<P, Q>(prm, s, ks);  // ends with __syncthreads
   const float* Us = ks;
   const float* Vs = ks + KL.offV;
@@ -445,7 +462,7 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_bwd_kernel(PtsPar
     if (has && end > beg)  // the cell's homogeneous control points -> smem
       for (int e = gl; e < NC; e += kGrp) {
         const int r = e / (Q + 1), h = e - r * (Q + 1);
-        cqg[e] = homog(__ldg(ctrl_s + (cu + r) * m + cv + h));
+        cqg[e] = prm.ctrl_smem ? net[(cu + r) * m + cv + h] : homog(__ldg(ctrl_s + (cu + r) * m + cv + h));
       }
     __syncwarp();
     float ru[RU], rv[RV];  // the cell's span records, in registers for all its points

@@ -14,6 +14,7 @@ struct PtsPlan {
   int chunk_b, nchunk_b;   // backward
   size_t smem_f, smem_b;   // dynamic smem bytes
   int ctrl_smem;           // forward stages the homogeneous net in smem
+  int ctrl_smem_b;         // backward stages the homogeneous net in smem
   bool fits_f, fits_b;     // smem within kPtsSmemMax (bwd also: cells <= 65535)
   size_t ws_bytes;         // backward chunk partials (nchunk_b > 1)
 };
