@@ -1165,6 +1165,9 @@ def run_grid(args, rank, world, local):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * K,
+            **({"plumbing_only": f"NB_BENCH_SHARE_GPU=1: {world} ranks on {torch.cuda.device_count()} GPU(s) with a "
+                                 "gloo group; checks the N-rank launch, sharding and reduction path, the timings are "
+                                 "not scaling numbers"} if share else {}),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
