@@ -4,6 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2104_14547_b200.build import build
 VARIANTS = {
     "base": [],
+    "cur": [],
+    "nospan": ["-DNB_NO_SPANWALK"],
     "unrolladv": ["-DNB_EXP_UNROLL_ADV"],
     "rowcopies": ["-DNB_EXP_ROWCOPIES"],
     "t8192": ["-DNB_TARGET_CTAS=8192"],
