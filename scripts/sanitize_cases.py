@@ -79,6 +79,18 @@ def case_unsorted():
         surf(w, u=w.u[rng.permutation(w.n_u)].copy(), v=w.v[::-1].copy())
 
 
+def case_shard_plans():
+    """the round-2 plans: config 4 below kDirectMinB (tiled + reduce) and a config-5 u-slab on
+    its sub-net window (dist.row_window)"""
+    surf(wl.config4(B=20), tables=True)
+    from paper_2104_14547_b200 import dist as nbd
+    w = wl.config5(n_u=512, n_v=256)
+    a0, a1 = nbd.shard_range(w.n_u, 8, 3)
+    r0, r1 = nbd.row_window(w.U, w.p, w.n, float(w.u[a0]), float(w.u[a1 - 1]))
+    surf(wl.Surfaces(name="win", p=w.p, q=w.q, ctrl=w.ctrl[:, r0:r1].copy(), U=w.U[r0:r1 + w.p + 1].copy(),
+                     V=w.V, u=w.u[a0:a1].copy(), v=w.v), tables=True)
+
+
 CASES = {k[5:]: f for k, f in globals().items() if k.startswith("case_")}
 
 if __name__ == "__main__":
