@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   uint64_t* sfull = bars + 1;           // bwd: stage slot filled by TMA (count 1 + tx bytes)
   uint64_t* sempty = bars + 1 + NST;    // fwd: stage slot drained by TMA (count 1)
   int* scnt = reinterpret_cast<int*>(bars + 1 + 2 * NST);  // per slot: warps done with the stage
-  float* rowdot = reinterpret_cast<float*>(scnt + NST + 2);  // KG: [4 warps][kRowChunk][P+1]
+  // KG: [4 warps][kRowChunk][P+1], 16-byte aligned (the stage buffers behind it are read as float4)
+  float* rowdot = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(scnt + NST + 2) + 15) & ~uintptr_t(15));
 
   if (tid == 0) {
     mbar_init(band_bar, 1u);
@@ -543,7 +544,12 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   // p+1 dot products of the stage's rows in a per-warp buffer (row stride 33 floats: the
   // column reads below are bank-conflict free); at the end of the stage lane l sums one
   // (row, r) pair over the 32 lanes in lane order (deterministic) — no per-row shuffles.
-  constexpr int KGS = 33, KGR = 4;  // buffer row stride, rows per buffer fill
+  // KG: the warp sums of G . T_r per walk row -> rowdot[warp][ci][r]. Each lane parks its
+  // p+1 dot products of the stage's rows in a per-warp buffer (row stride 36 floats: 16-byte
+  // rows, conflict-free float4 reads); every KGR rows, two lanes sum one (row, r) pair's 32
+  // lane values — 16 each as four float4 in a fixed tree — and one xor shuffle joins the
+  // halves (deterministic, all 32 lanes busy).
+  constexpr int KGS = 36, KGR = 4;  // buffer row stride, rows per buffer fill
   float* kgb = rowdot + (kThreads / 32) * kRowChunk * (P + 1) + warp * (KGR * (P + 1) * KGS);
   auto kg_row = [&](int ci, const float (&d)[P + 1]) {
     if constexpr (KG) {
@@ -555,13 +561,21 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   auto kg_stage = [&](int ci0, int nr) {
     if constexpr (KG) {
       __syncwarp();
-      for (int pr = lane; pr < nr * (P + 1); pr += 32) {
-        const float* src = kgb + pr * KGS;
+      const int npair = nr * (P + 1), half = lane & 1;
+      for (int base = 0; base < npair; base += 16) {  // uniform trip count (P > 3: two rounds)
+        const int pr = base + (lane >> 1);
         float v = 0.f;
-#pragma unroll 8
-        for (int j = 0; j < 32; ++j) v += src[j];
-        const int rr = pr / (P + 1), k = pr - rr * (P + 1);
-        rowdot[(warp * kRowChunk + ci0 + rr) * (P + 1) + k] = v;
+        if (pr < npair) {
+          const float4* src = reinterpret_cast<const float4*>(kgb + pr * KGS + half * 16);
+          const float4 a = src[0], b = src[1], c = src[2], d = src[3];
+          v = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
+              (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (half == 0 && pr < npair) {
+          const int rr = pr / (P + 1), k = pr - rr * (P + 1);
+          rowdot[(warp * kRowChunk + ci0 + rr) * (P + 1) + k] = v;
+        }
       }
       __syncwarp();
     }

@@ -172,7 +172,7 @@ size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg, boo
   b += 4 * 4;                                  // misc
   b = (b + 7) / 8 * 8 + (1 + 2 * nst) * 8 + nst * 4;  // mbarriers + stage counters
   if (kg)  // rowdot + the per-warp stage buffers of the row dot products (NEXT-4)
-    b += 8 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4 + (size_t)(kThreads / 32) * 4 * (P + 1) * 33 * 4;
+    b += 16 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4 + (size_t)(kThreads / 32) * 4 * (P + 1) * 36 * 4;
   return b;
 }
 
