@@ -117,8 +117,9 @@ int    nurbs_surface_bwd(const nurbs_shape* shape, const float* ctrl,
                          void* workspace, size_t ws_bytes, void* stream);
 size_t nurbs_surface_bwd_workspace_bytes(const nurbs_shape* shape);
 
-/* Diagnostic: the launch plan the grid kernels use for `shape` (a pure function of the
- * shape, which is what makes results bitwise repeatable). Writes plan[0..5] = K (knot spans
+/* Diagnostic: the launch plan of the backward / fitting step for `shape` (a pure function of
+ * the shape, which is what makes results bitwise repeatable; the forward, which has no
+ * reduction, picks its own row blocks by a wave model). Writes plan[0..5] = K (knot spans
  * of u per row block), row blocks, column blocks (128 samples of v each), control rows per
  * band, 1 if one tile per surface (no cross-tile reduction) else 0, CTAs per launch
  * (saturated at INT32_MAX). Curves (m = 1, q = 0) are planned as one row of the grid.
