@@ -106,6 +106,25 @@ def test_plan_is_bounded(lib):
     assert lib.nurbs_grid_plan(None, (ctypes.c_int32 * 6)()) == 1
 
 
+def test_plan_rules_at_the_measured_shapes(lib):
+    """The backward plan's fitted rules (profiles/r02_plan_sweep.txt) at the shapes
+    they were fitted on: one tile per surface for config 4 from B = 128 surfaces up (every
+    per-rank shard of the 1..8-GPU runs), tiled below; config 5 and its sub-net windows take
+    the sweep's best K (7, and 4 for the 8-way window)."""
+    from paper_2104_14547_b200 import _abi, api
+    cfg4 = lambda B: api.grid_plan(_abi.nurbs_shape(B, 16, 16, 3, 3, 128, 128, 0))  # noqa: E731
+    for B in (4096, 2048, 1024, 512, 128):
+        assert cfg4(B)["direct"] == 1 and cfg4(B)["K"] == 13
+    assert cfg4(127)["direct"] == 0 and cfg4(1)["direct"] == 0
+    assert api.grid_plan(_abi.nurbs_shape(1, 256, 256, 3, 3, 8192, 8192, 0))["K"] == 7
+    assert api.grid_plan(_abi.nurbs_shape(1, 131, 256, 3, 3, 4096, 8192, 0))["K"] == 7    # G = 2 window
+    assert api.grid_plan(_abi.nurbs_shape(1, 68, 256, 3, 3, 2048, 8192, 0))["K"] == 7     # G = 4
+    assert api.grid_plan(_abi.nurbs_shape(1, 36, 256, 3, 3, 1024, 8192, 0))["K"] == 4     # G = 8
+    # configs 2 and 3 (latency-bound; a K sweep: K = 1 fastest)
+    assert api.grid_plan(_abi.nurbs_shape(1, 8, 8, 3, 3, 64, 64, 0))["K"] == 1
+    assert api.grid_plan(_abi.nurbs_shape(1, 32, 32, 3, 3, 512, 512, 0))["K"] == 1
+
+
 def test_binding_rejects_wrong_dtypes_and_sizes():
     """The Python binding checks dtype and element counts before any pointer reaches the C
     ABI (a wrong size would read out of bounds, a float64 tensor would be reinterpreted)."""

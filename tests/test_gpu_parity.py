@@ -481,16 +481,18 @@ def test_config5_full_size():
 
 
 # --------------------------------------------------------------------------- per-rank shard shapes
-@pytest.mark.parametrize("B", [512, 100])
+@pytest.mark.parametrize("B", [512, 100, 128, 127, 3])
 def test_config4_rank_shard_plans(B):
-    """Config 4's per-rank batch at G = 8 (B = 512: one tile per surface) and a batch below
-    kDirectMinB (B = 100: tiled plan + cross-tile reduce), in the bench launch configuration
-    (tables), against the fp64 oracle (every surface for B = 100, 32 sampled for B = 512)."""
+    """Config 4's per-rank batch at G = 8 (B = 512: one tile per surface), the direct/tiled
+    switch of the plan (B = 128 direct, 127 tiled + cross-tile reduce) and small batches, in the
+    bench launch configuration (tables), against the fp64 oracle (every surface up to 128, 32
+    sampled for B = 512); the gradient is bitwise repeatable."""
     w = wl.config4(B=B)
     g = w.grad_out(11)
     pl = nb.grid_plan(nb.nurbs_shape(B, 16, 16, 3, 3, 128, 128, 0))
     assert pl["direct"] == (1 if B >= 128 else 0)
     out, grad = run_surface(w, g, tables=True)
+    np.testing.assert_array_equal(grad, run_surface(w, g, tables=True)[1])
     idx = np.arange(B) if B <= 128 else np.random.default_rng(3).choice(B, 32, replace=False)
     c = w.ctrl[idx]
     ro = oracle.surface_fwd(c, w.U, w.V, w.u, w.v, w.p, w.q)
