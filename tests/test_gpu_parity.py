@@ -625,6 +625,33 @@ def test_surface_derivs_parity(case):
     assert np.min(cos) >= 1 - 1e-4
 
 
+def test_surface_derivs_full_cfg4_sampled():
+    """The derivative kernel in the bench launch configuration (config 4: 4096 surfaces, 128^2):
+    32 sampled whole surfaces against the fp64 oracle (S, S_u, S_v, normals), every normal of
+    the batch of unit length, and S equal to the grid forward's within the forward tolerance."""
+    w = wl.config4()
+    ctrl, U, V, u, v = T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v)
+    S, Su, Sv, nrm = nb.surface_derivs(ctrl, U, V, u, v, w.p, w.q)
+    Sf = nb.surface_fwd(ctrl, U, V, u, v, w.p, w.q)
+    torch.cuda.synchronize()
+    nlen = torch.linalg.vector_norm(nrm, dim=-1)
+    assert float((nlen - 1).abs().max()) <= 1e-5
+    idx = np.random.default_rng(9).choice(w.B, 32, replace=False)
+    c = w.ctrl[idx]
+    Sn = S.cpu().numpy()
+    assert fwd_err(Sn, Sf.cpu().numpy(), w.ctrl) <= FWD_TOL
+    parts = oracle.pmap(lambda k0, k1: oracle.surface_derivs(c[k0:k1], w.U, w.V, w.u, w.v, w.p, w.q),
+                        [(k, k + 4) for k in range(0, 32, 4)])
+    rS, rSu, rSv = (np.concatenate([pt[j] for pt in parts]) for j in range(3))
+    assert fwd_err(Sn[idx], rS, c, "derivs cfg4 full") <= FWD_TOL
+    e_u, e_v = der_err(Su.cpu().numpy()[idx], rSu), der_err(Sv.cpu().numpy()[idx], rSv)
+    record("derivs cfg4 full", "Su", e_u); record("derivs cfg4 full", "Sv", e_v)
+    assert e_u <= DER_TOL and e_v <= DER_TOL
+    rn = np.cross(rSu, rSv)
+    rn /= np.linalg.norm(rn, axis=-1, keepdims=True)
+    assert np.min(np.sum(nrm.cpu().numpy()[idx] * rn, axis=-1)) >= 1 - 1e-4
+
+
 def test_cylinder_normals_on_gpu():
     s2 = np.float32(np.sqrt(2.0) / 2.0)
     arc = [((1, 0), 1.0), ((1, 1), s2), ((0, 1), 1.0)]
