@@ -119,7 +119,7 @@ Geo curve_geo(const nurbs_shape* sh, const float* U, const float* u) {
 // tables built for another n, degree or sample count would be read at wrong offsets.
 int attach_tables(Geo& g, const void* tables, cudaStream_t st) {
   if (!tables) return NURBS_OK;
-  const nb::TabLayout L = nb::tab_layout(g.P > 0 ? g.r.ns : 0, g.r.p, g.c.ns, g.c.p);
+  const nb::TabLayout L = nb::tab_layout(g.P > 0 ? g.r.ns : 0, g.r.p, g.c.ns, g.c.p, g.r.n);
   const unsigned char* t = static_cast<const unsigned char*>(tables);
   if (check_mode()) {
     int h[10] = {};
@@ -137,6 +137,7 @@ int attach_tables(Geo& g, const void* tables, cudaStream_t st) {
     g.r.tspan = reinterpret_cast<const int*>(t + L.off_span_r);
     g.r.tN = reinterpret_cast<const float*>(t + L.off_N_r);
     g.r.tnp = L.np_r;
+    g.r.tsfirst = L.nsf_r > 0 ? reinterpret_cast<const int*>(t + L.off_sfirst_r) : nullptr;
   }
   g.c.tspan = reinterpret_cast<const int*>(t + L.off_span_c);
   g.c.tN = reinterpret_cast<const float*>(t + L.off_N_c);
@@ -634,8 +635,8 @@ const char* nurbs_last_error_detail(void) { return g_detail.c_str(); }
 
 size_t nurbs_tables_bytes(const nurbs_shape* sh) {
   if (!sh) return 0;
-  if (sh->m == 1 && sh->q == 0) return nb::tab_layout(0, 0, sh->n_u, sh->p).bytes;
-  return nb::tab_layout(sh->n_u, sh->p, sh->n_v, sh->q).bytes;
+  if (sh->m == 1 && sh->q == 0) return nb::tab_layout(0, 0, sh->n_u, sh->p, 1).bytes;
+  return nb::tab_layout(sh->n_u, sh->p, sh->n_v, sh->q, sh->n).bytes;
 }
 
 int nurbs_tables(const nurbs_shape* sh, const float* U, const float* V, const float* u, const float* v,
@@ -666,7 +667,7 @@ int nurbs_tables(const nurbs_shape* sh, const float* U, const float* V, const fl
   }
   Dir r = g.r;
   if (curve) r.ns = 0;
-  const nb::TabLayout L = nb::tab_layout(r.ns, r.p, g.c.ns, g.c.p);
+  const nb::TabLayout L = nb::tab_layout(r.ns, r.p, g.c.ns, g.c.p, r.n);
   cudaError_t e = nb::launch_tables(r, g.c, tables, L, s);
   if (e != cudaSuccess) return cuda_fail(e, "tables kernel launch");
   return NURBS_OK;

@@ -284,7 +284,10 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
 
   // ---- sample rows of this row block: spans in [S0, S1)
   int a_lo = 0, a_hi = R.ns;
-  if (prm.NRB > 1) {
+  if (prm.NRB > 1 && R.tsfirst) {  // tables: the row block's first / past-last sample, two loads
+    if (rb > 0) a_lo = min(max(__ldg(R.tsfirst + (S0 - P)), 0), R.ns);
+    if (rb < prm.NRB - 1) a_hi = min(max(__ldg(R.tsfirst + (S1 - P)), a_lo), R.ns);
+  } else if (prm.NRB > 1) {
     int s_end = R.n - 1;  // last non-empty span (R3)
     if (P > 0 && !R.tspan)
       while (s_end > P && __ldg(Uk + s_end) == __ldg(Uk + s_end + 1)) --s_end;
@@ -803,8 +806,8 @@ static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
-  nurbs_grid_kernel<P, Q, BWD, IO, FIT, KG>
-      <<<(unsigned)((long long)prm.B * prm.NRB * prm.NCB), kThreads, smem, st>>>(prm);
+  const unsigned grid = (unsigned)((long long)prm.B * prm.NRB * prm.NCB);
+  nurbs_grid_kernel<P, Q, BWD, IO, FIT, KG><<<grid, kThreads, smem, st>>>(prm);
   return cudaGetLastError();
 }
 

@@ -69,6 +69,7 @@ struct Dir {
   const int* tspan;         // optional tables: span per sample
   const float* tN;          // optional tables: basis per sample, tnp floats each
   int tnp;
+  const int* tsfirst;       // optional tables (rows): first sample with span >= s, at s - p
 };
 
 struct Params {
@@ -107,25 +108,29 @@ struct Params {
 };
 constexpr int kBoxCols = 64;             // sample columns per tensor box (192 floats)
 
-// Tables blob layout (nurbs_tables): header then four arrays, each 256-byte aligned.
+// Tables blob layout (nurbs_tables): header then five arrays, each 256-byte aligned; the
+// last, sfirst_r[s - p] (s = p..n), is the first row sample whose knot span is >= s: a row
+// block's sample range in two loads instead of a CTA-wide search.
 struct TabLayout {
-  size_t off_span_r, off_N_r, off_span_c, off_N_c, bytes;
-  int np_r, np_c;
+  size_t off_span_r, off_N_r, off_span_c, off_N_c, off_sfirst_r, bytes;
+  int np_r, np_c, nsf_r;
 };
 
 inline int basis_stride(int p) { return (p + 1) <= 4 ? 4 : 8; }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-inline TabLayout tab_layout(int ns_r, int p_r, int ns_c, int p_c) {
+inline TabLayout tab_layout(int ns_r, int p_r, int ns_c, int p_c, int n_r) {
   TabLayout L;
   L.np_r = basis_stride(p_r);
   L.np_c = basis_stride(p_c);
+  L.nsf_r = (ns_r > 0 && p_r > 0 && n_r > p_r) ? n_r - p_r + 1 : 0;
   size_t o = 256;  // header
   L.off_span_r = o; o = align_up(o + sizeof(int) * (size_t)ns_r, 256);
   L.off_N_r = o;    o = align_up(o + sizeof(float) * (size_t)ns_r * L.np_r, 256);
   L.off_span_c = o; o = align_up(o + sizeof(int) * (size_t)ns_c, 256);
   L.off_N_c = o;    o = align_up(o + sizeof(float) * (size_t)ns_c * L.np_c, 256);
+  L.off_sfirst_r = o; o = align_up(o + sizeof(int) * (size_t)L.nsf_r, 256);
   L.bytes = o;
   return L;
 }

@@ -116,6 +116,13 @@ __global__ void nurbs_tables_kernel(Dir R, Dir C, unsigned char* tab, TabLayout 
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     if (k < np) N[(size_t)a * np + k] = (k <= D.p && k <= kMaxQ) ? nb_[k <= kMaxQ ? k : 0] : 0.f;
+  if (idx < R.ns && L.nsf_r > 0) {  // sfirst[s - p] = a for the spans s in (span(a-1), span(a)]
+    int* sf = reinterpret_cast<int*>(tab + L.off_sfirst_r);
+    const int prev = a > 0 ? d_find_span(D.knots, D.n, D.p, __ldg(D.s + a - 1)) : D.p - 1;
+    for (int k = max(prev + 1, D.p); k <= min(sp, D.n); ++k) sf[k - D.p] = a;
+    if (a == R.ns - 1)  // spans past the last sample's
+      for (int k = max(sp + 1, D.p); k <= D.n; ++k) sf[k - D.p] = R.ns;
+  }
 }
 
 // ------------------------------------------------------------------------ validation
