@@ -712,7 +712,7 @@ def run_paired(args, rank, world):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        nbd.init_nccl(dev)
     full = wl.config4_paired(seed=41)
     b0, b1 = nbd.shard_range(full.B, world, rank) if world > 1 else (0, full.B)
     T_ = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
@@ -889,12 +889,10 @@ def run_grid(args, rank, world, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        if args.config == 5 and not args.ordered_reduce:
-            nbd.pin_nccl_order()
         if share:
             dist.init_process_group("gloo")
         else:
-            dist.init_process_group("nccl", device_id=dev)
+            nbd.init_nccl(dev)   # async error handling + timeout; all-reduce order pinned
     assert args.warmup >= 3, "timing rules need >= 3 warm-up steps"
     if args.tc:
         nb.path_flags(tc=True).__enter__()

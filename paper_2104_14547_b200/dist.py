@@ -102,6 +102,19 @@ class OrderedReducer:
         self.sum_fn(self.gathered.view(self.world, -1), buf.flat)
 
 
+def init_nccl(device, timeout_s: float = 120.0) -> None:
+    """One process per GPU over NCCL with failure detection: NCCL's asynchronous error handling
+    on (a rank that hits a communicator error or a collective that exceeds `timeout_s` aborts
+    the process group and raises instead of hanging the job), order pinned for the gradient
+    all-reduce (pin_nccl_order). Call once per rank; RANK / WORLD_SIZE / MASTER_* from the
+    environment (torch.distributed.run)."""
+    import datetime
+    import os
+    os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+    pin_nccl_order()
+    dist.init_process_group("nccl", device_id=device, timeout=datetime.timedelta(seconds=timeout_s))
+
+
 def allreduce_grads(buf: GradBuffer, group=None, reducer: "OrderedReducer | None" = None) -> None:
     """Sum the per-rank partial gradients: one NCCL all-reduce over NVLink / NVSwitch (order
     fixed by pin_nccl_order), or, with an OrderedReducer, all-gather + rank-order sum."""

@@ -185,3 +185,18 @@ def test_pin_nccl_order_keeps_caller_settings(monkeypatch):
     monkeypatch.delenv("NCCL_ALGO", raising=False)
     monkeypatch.setenv("NCCL_PROTO", "LL128")
     assert nbd.pin_nccl_order() == {"NCCL_ALGO": "Ring", "NCCL_PROTO": "LL128"}
+
+
+def test_init_nccl_sets_failure_detection(monkeypatch):
+    """init_nccl turns on NCCL's asynchronous error handling, pins the reduction order and
+    passes a collective timeout (the process-group call itself is stubbed: no GPU here)."""
+    import datetime
+    calls = {}
+    monkeypatch.delenv("TORCH_NCCL_ASYNC_ERROR_HANDLING", raising=False)
+    monkeypatch.delenv("NCCL_ALGO", raising=False)
+    monkeypatch.delenv("NCCL_PROTO", raising=False)
+    monkeypatch.setattr(nbd.dist, "init_process_group", lambda backend, **kw: calls.update(backend=backend, **kw))
+    nbd.init_nccl("cuda:0", timeout_s=30.0)
+    assert calls["backend"] == "nccl" and calls["timeout"] == datetime.timedelta(seconds=30)
+    assert os.environ["TORCH_NCCL_ASYNC_ERROR_HANDLING"] == "1"
+    assert os.environ["NCCL_ALGO"] == "Ring" and os.environ["NCCL_PROTO"] == "Simple"
