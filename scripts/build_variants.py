@@ -17,6 +17,11 @@ VARIANTS = {
     "expopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "t1184": ["-DNB_TARGET_CTAS=1184"],
     "nob2": ["-DNB_EXP_NO_B2"],
+    "ptspk": [],
+    "ptsnopk": ["-DNB_PTS_NO_PACKED_BASIS"],
+    "ptsg4": ["-DNB_KGRP=4"],
+    "ptsf2": ["-DNB_KGRPF=2"],
+    "ptsg4f8": ["-DNB_KGRP=4", "-DNB_KGRPF=8"],
     "b2sync": ["-DNB_EXP_B2_NOSYNC_WORK"],
     "st2": ["-DNB_STAGES_B=2"],
     "minb3": ["-DNB_MINB_B=3"],

@@ -80,9 +80,15 @@ def main():
                   if "warps_issue_stalled" in k and k.endswith("per_issue_active.ratio") and d[k]]
             st = sorted([x for x in st if x[1] > 0.1], key=lambda x: -x[1])
             lines.append("    stalls per issue: " + ", ".join(f"{k} {v:.2f}" for k, v in st))
-            targs = d["Kernel Name"].split("<", 1)[1].split(">", 1)[0].replace("(int)", "").replace("(bool)", "")
+            kn = d["Kernel Name"]
+            if "<" not in kn:  # untemplated helper kernels (reduce, validate): no traffic entry
+                continue
+            targs = kn.split("<", 1)[1].split(">", 1)[0].replace("(int)", "").replace("(bool)", "")
             targs = [x.strip() for x in targs.split(",")]
-            kind = "bwd" if len(targs) > 2 and targs[2] in ("1", "true") else "fwd"  # <P, Q, BWD, ...>
+            if "points_" in kn:
+                kind = "bwd" if "bwd" in kn else "fwd"
+            else:
+                kind = "bwd" if len(targs) > 2 and targs[2] in ("1", "true") else "fwd"  # <P, Q, BWD, ...>
             traffic.setdefault(f"cfg{a.cfg}", {})[kind] = {"kernel": name, "dram_bytes_per_launch": (rd + wr) * 1e6,
                                                           "source": os.path.basename(a.full), "tag": a.tag}
         json.dump(traffic, open(traffic_path, "w"), indent=1)
