@@ -481,9 +481,10 @@ __global__ void __launch_bounds__(kPtsThreads, 2) nurbs_points_bwd_kernel(PtsPar
   const float4* ctrl_s = prm.ctrl + (size_t)s * nm;
 #ifndef NB_PTS_NO_PREFETCH
   if (tid == 0 && cnt > 0) {  // the chunk's dL/dS into L2 while the points are sorted (pass 4 gathers it)
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(g) & ~uintptr_t(15);
-    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(g + 3 * (size_t)cnt) + 15) & ~uintptr_t(15);
-    prefetch_l2_bulk(reinterpret_cast<const void*>(a0), (uint32_t)(a1 - a0));
+    // 16-byte granules inside [g, g + 3 cnt) only (a prefetch never touches bytes past the data)
+    const uintptr_t a0 = (reinterpret_cast<uintptr_t>(g) + 15) & ~uintptr_t(15);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(g + 3 * (size_t)cnt) & ~uintptr_t(15);
+    if (a1 > a0) prefetch_l2_bulk(reinterpret_cast<const void*>(a0), (uint32_t)(a1 - a0));
   }
 #endif
 
