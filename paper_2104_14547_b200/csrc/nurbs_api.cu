@@ -2,6 +2,7 @@
 // launch plan, checked mode, and the kernel launches on the caller's stream.
 // Citations: P:n = reference/PAPER.md line n; R<k> = DESIGN.md §3 reading k.
 #include <atomic>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -353,6 +354,32 @@ KnotWs knot_ws(const Geo& g, const Plan& pl) {
   return w;
 }
 
+// A helper stream per device for the column-direction knot assembly: the two directions'
+// assembly chains (a few small, latency-bound kernels each, nurbs_knots.cu) are independent,
+// so the v chain runs beside the u chain. Fork / join through events: the call stays
+// asynchronous on the caller's stream and CUDA-graph capturable. The mutex keeps one call's
+// event record / wait pairs together when several host threads share a device.
+struct AsmSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_asm_mu;
+AsmSide g_asm[64];
+cudaError_t asm_side(AsmSide*& out) {  // call with g_asm_mu held
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  AsmSide& a = g_asm[dev];
+  if (!a.s) {
+    if ((e = cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  out = &a;
+  return cudaSuccess;
+}
+
 int launch_knots(const Geo& g, const float* ctrl, const float* gout, float* gctrl, float* gR, float* gC, void* ws,
                  size_t ws_bytes, cudaStream_t st) {
   const Plan pl = nb::make_plan(g.B, g.r.n, g.P, g.r.ns, g.c.n, g.c.ns);
@@ -396,18 +423,34 @@ int launch_knots(const Geo& g, const float* ctrl, const float* gout, float* gctr
   cudaError_t e = nb::launch_grid(prm, 3, g.P, g.c.p, st);
   if (e != cudaSuccess) return cuda_fail(e, "backward (knot gradients) kernel launch");
   if (!pl.direct && (e = nb::launch_reduce(prm, g.P, st)) != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
-  if (g.P > 0 && gR) {
-    nb::KnotDir d{g.B, g.r.n, g.P, g.r.ns, g.r.knots, g.r.kstride, g.r.s, g.r.tspan, prm.hU, pl.NCB,
-                  reinterpret_cast<float*>(w + W.cR), reinterpret_cast<int*>(w + W.sR)};
-    e = nb::launch_knot_grad(d, g.r.kstride != 0, reinterpret_cast<float*>(w + W.tR), gR, st);
-    if (e != cudaSuccess) return cuda_fail(e, "knot-gradient kernels (u)");
-  }
-  if (gC) {
+  const bool doR = g.P > 0 && gR;
+  auto chain_v = [&](cudaStream_t sv) {
     nb::KnotDir d{g.B, g.c.n, g.c.p, g.c.ns, g.c.knots, g.c.kstride, g.c.s, g.c.tspan, prm.hV, pl.NRB,
                   reinterpret_cast<float*>(w + W.cC), reinterpret_cast<int*>(w + W.sC)};
-    e = nb::launch_knot_grad(d, g.c.kstride != 0, reinterpret_cast<float*>(w + W.tC), gC, st);
-    if (e != cudaSuccess) return cuda_fail(e, "knot-gradient kernels (v)");
+    return nb::launch_knot_grad(d, g.c.kstride != 0, reinterpret_cast<float*>(w + W.tC), gC, sv);
+  };
+  auto chain_u = [&](cudaStream_t su) {
+    nb::KnotDir d{g.B, g.r.n, g.P, g.r.ns, g.r.knots, g.r.kstride, g.r.s, g.r.tspan, prm.hU, pl.NCB,
+                  reinterpret_cast<float*>(w + W.cR), reinterpret_cast<int*>(w + W.sR)};
+    return nb::launch_knot_grad(d, g.r.kstride != 0, reinterpret_cast<float*>(w + W.tR), gR, su);
+  };
+  if (doR && gC) {  // both directions: the v chain on the helper stream, forked after the grid kernel
+    std::lock_guard<std::mutex> lk(g_asm_mu);
+    AsmSide* a = nullptr;
+    if ((e = asm_side(a)) != cudaSuccess) return cuda_fail(e, "knot-gradient helper stream");
+    if ((e = cudaEventRecord(a->fork, st)) != cudaSuccess) return cuda_fail(e, "knot-gradient fork");
+    if ((e = cudaStreamWaitEvent(a->s, a->fork, 0)) != cudaSuccess) return cuda_fail(e, "knot-gradient fork");
+    const cudaError_t ev = chain_v(a->s);
+    // join even after a failed launch, so a capturing caller's graph is never left forked
+    if ((e = cudaEventRecord(a->join, a->s)) != cudaSuccess) return cuda_fail(e, "knot-gradient join");
+    const cudaError_t eu = chain_u(st);
+    if ((e = cudaStreamWaitEvent(st, a->join, 0)) != cudaSuccess) return cuda_fail(e, "knot-gradient join");
+    if (ev != cudaSuccess) return cuda_fail(ev, "knot-gradient kernels (v)");
+    if (eu != cudaSuccess) return cuda_fail(eu, "knot-gradient kernels (u)");
+    return NURBS_OK;
   }
+  if (doR && (e = chain_u(st)) != cudaSuccess) return cuda_fail(e, "knot-gradient kernels (u)");
+  if (gC && (e = chain_v(st)) != cudaSuccess) return cuda_fail(e, "knot-gradient kernels (v)");
   return NURBS_OK;
 }
 

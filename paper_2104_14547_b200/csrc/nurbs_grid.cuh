@@ -72,7 +72,11 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
     const float4 G = make_float4(gxy.x, gxy.y, gzr, -gS * rw);
 #pragma unroll
     for (int k = 0; k <= P; ++k) acc[k] = fma4v(nu[k], G, acc[k]);
+#ifdef NB_EXP_KG_NOROW
+    if constexpr (false) {
+#else
     if constexpr (KG) {  // NEXT-4: G . T_r, the row's weight of dN_r/dU
+#endif
 #pragma unroll
       for (int k = 0; k <= P; ++k) {
         const float2 t2 = up2(ffma2(pk2(G.z, G.w), pk2(tw[k].z, tw[k].w), fmul2(pk2(G.x, G.y), pk2(tw[k].x, tw[k].y))));
@@ -555,14 +559,22 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   constexpr int KGS = 36, KGR = 4;  // buffer row stride, rows per buffer fill
   float* kgb = rowdot + (kThreads / 32) * kRowChunk * (P + 1) + warp * (KGR * (P + 1) * KGS);
   auto kg_row = [&](int ci, const float (&d)[P + 1]) {
+#ifdef NB_EXP_KG_NOROW
+    if constexpr (false) {
+#else
     if constexpr (KG) {
+#endif
       const int rr = ci % KGR;
 #pragma unroll
       for (int k = 0; k <= P; ++k) kgb[(rr * (P + 1) + k) * KGS + lane] = d[k];
     }
   };
   auto kg_stage = [&](int ci0, int nr) {
+#ifdef NB_EXP_KG_NOROW
+    if constexpr (false) {
+#else
     if constexpr (KG) {
+#endif
       __syncwarp();
       const int npair = nr * (P + 1), half = lane & 1;
       for (int base = 0; base < npair; base += 16) {  // uniform trip count (P > 3: two rounds)

@@ -15,6 +15,43 @@
 
 namespace nb {
 
+// sum_r dN_r(u)/dU[s-p+1+t] * h[r] for one t in [0, 2p): the A2.2 triangle with dual numbers
+// along knot t. kn = U[s-p+1 .. s+p].
+template <int P>
+__device__ __forceinline__ float d_basis_dknot_one(const float (&kn)[2 * P], float u, const float (&h)[P + 1],
+                                                   int t) {
+  float N[P + 1], D[P + 1], left[P + 1], right[P + 1], dl[P + 1], dr[P + 1];
+  N[0] = 1.f;
+  D[0] = 0.f;
+#pragma unroll
+  for (int j = 1; j <= P; ++j) {
+    left[j] = u - kn[P - j];            // u - U[s+1-j]
+    dl[j] = (P - j == t) ? -1.f : 0.f;
+    right[j] = kn[P - 1 + j] - u;       // U[s+j] - u
+    dr[j] = (P - 1 + j == t) ? 1.f : 0.f;
+    float saved = 0.f, dsaved = 0.f;
+#pragma unroll
+    for (int r = 0; r < j; ++r) {
+      const float den = right[r + 1] + left[j - r];
+      const float dden = dr[r + 1] + dl[j - r];
+      const float temp = N[r] / den;
+      const float dtemp = (D[r] - temp * dden) / den;
+      const float nN = fmaf(right[r + 1], temp, saved);
+      const float nD = dsaved + dr[r + 1] * temp + right[r + 1] * dtemp;
+      saved = left[j - r] * temp;
+      dsaved = dl[j - r] * temp + left[j - r] * dtemp;
+      N[r] = nN;
+      D[r] = nD;
+    }
+    N[j] = saved;
+    D[j] = dsaved;
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int r = 0; r <= P; ++r) acc = fmaf(D[r], h[r], acc);
+  return acc;
+}
+
 // c[t] = sum_r dN_r(u)/dU[s-p+1+t] * h[r], t = 0..2p-1 (A2.2 with dual numbers, one pass per knot).
 template <int P>
 __device__ __forceinline__ void d_basis_dknots(const float* __restrict__ U, int s, float u, const float (&h)[P + 1],
@@ -23,38 +60,32 @@ __device__ __forceinline__ void d_basis_dknots(const float* __restrict__ U, int 
 #pragma unroll
   for (int t = 0; t < 2 * P; ++t) kn[t] = __ldg(U + s - P + 1 + t);
 #pragma unroll
-  for (int t = 0; t < 2 * P; ++t) {
-    float N[P + 1], D[P + 1], left[P + 1], right[P + 1], dl[P + 1], dr[P + 1];
-    N[0] = 1.f;
-    D[0] = 0.f;
+  for (int t = 0; t < 2 * P; ++t) c[t] = d_basis_dknot_one<P>(kn, u, h, t);
+}
+
+// Single-part weights (nparts == 1, e.g. the batch-summed weights of shared knots): one thread
+// per (surface, sample, knot t) instead of per sample — the 2p dual passes run in parallel
+// (the per-sample pass chain is what bounds this kernel's latency). Same arithmetic per t.
+template <int P>
+__global__ void nurbs_knot_rows_t_kernel(KnotDir d) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)d.B * d.ns * (2 * P)) return;
+  const long long sa = idx / (2 * P);
+  const int t = (int)(idx - sa * (2 * P));
+  const int s = (int)(sa / d.ns), a = (int)(sa - (long long)s * d.ns);
+  float h[P + 1];
+  const float* src = d.part + ((size_t)s * d.ns + a) * (P + 1);
 #pragma unroll
-    for (int j = 1; j <= P; ++j) {
-      left[j] = u - kn[P - j];            // u - U[s+1-j]
-      dl[j] = (P - j == t) ? -1.f : 0.f;
-      right[j] = kn[P - 1 + j] - u;       // U[s+j] - u
-      dr[j] = (P - 1 + j == t) ? 1.f : 0.f;
-      float saved = 0.f, dsaved = 0.f;
+  for (int r = 0; r <= P; ++r) h[r] = __ldg(src + r);
+  const float* Uk = d.knots + (long long)s * d.kstride;
+  const float ua = __ldg(d.samples + a);
+  int sp = d.tspan ? __ldg(d.tspan + a) : d_find_span(Uk, d.n, P, ua);
+  sp = min(max(sp, P), d.n - 1);
+  float kn[2 * P];
 #pragma unroll
-      for (int r = 0; r < j; ++r) {
-        const float den = right[r + 1] + left[j - r];
-        const float dden = dr[r + 1] + dl[j - r];
-        const float temp = N[r] / den;
-        const float dtemp = (D[r] - temp * dden) / den;
-        const float nN = fmaf(right[r + 1], temp, saved);
-        const float nD = dsaved + dr[r + 1] * temp + right[r + 1] * dtemp;
-        saved = left[j - r] * temp;
-        dsaved = dl[j - r] * temp + left[j - r] * dtemp;
-        N[r] = nN;
-        D[r] = nD;
-      }
-      N[j] = saved;
-      D[j] = dsaved;
-    }
-    float acc = 0.f;
-#pragma unroll
-    for (int r = 0; r <= P; ++r) acc = fmaf(D[r], h[r], acc);
-    c[t] = acc;
-  }
+  for (int k = 0; k < 2 * P; ++k) kn[k] = __ldg(Uk + sp - P + 1 + k);
+  d.contrib[(size_t)sa * (2 * P) + t] = d_basis_dknot_one<P>(kn, ua, h, t);
+  if (t == 0) d.span[sa] = sp;
 }
 
 // Per (surface, sample): h = sum over the nparts partials (ascending), then the 2p knot
@@ -186,6 +217,18 @@ __global__ void __launch_bounds__(256) nurbs_knot_htree_kernel(const float* __re
 
 static cudaError_t launch_rows(const KnotDir& d, cudaStream_t st) {
   const long long rows = (long long)d.B * d.ns;
+  if (d.nparts == 1) {
+    const unsigned nbt = (unsigned)((rows * 2 * d.p + 127) / 128);
+    switch (d.p) {
+      case 1: nurbs_knot_rows_t_kernel<1><<<nbt, 128, 0, st>>>(d); break;
+      case 2: nurbs_knot_rows_t_kernel<2><<<nbt, 128, 0, st>>>(d); break;
+      case 3: nurbs_knot_rows_t_kernel<3><<<nbt, 128, 0, st>>>(d); break;
+      case 4: nurbs_knot_rows_t_kernel<4><<<nbt, 128, 0, st>>>(d); break;
+      case 5: nurbs_knot_rows_t_kernel<5><<<nbt, 128, 0, st>>>(d); break;
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+  }
   const unsigned nbk = (unsigned)((rows + 127) / 128);
   switch (d.p) {
     case 1: nurbs_knot_rows_kernel<1><<<nbk, 128, 0, st>>>(d); break;

@@ -17,6 +17,8 @@ VARIANTS = {
     "expopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "t1184": ["-DNB_TARGET_CTAS=1184"],
     "nob2": ["-DNB_EXP_NO_B2"],
+    "kgnorow": ["-DNB_EXP_KG_NOROW"],
+    "kasm": [],
     "ptspk": [],
     "ptsnopk": ["-DNB_PTS_NO_PACKED_BASIS"],
     "ptsg4": ["-DNB_KGRP=4"],
