@@ -120,3 +120,35 @@ def test_knot_grad_full_cfg4_batched_sampled():
         sub = wl.Surfaces("s", 3, 3, w.ctrl[k:k + 1], w.U[k:k + 1], w.V[k:k + 1], w.u, w.v, True)
         rU, rV = oracle.surface_knot_grad(sub.ctrl, sub.U, sub.V, sub.u, sub.v, g[k:k + 1], 3, 3, True)
         assert kerr(gU[k:k + 1], rU) <= KTOL and kerr(gV[k:k + 1], rV) <= KTOL
+
+
+@pytest.mark.parametrize("shared", [True, False])
+def test_knot_grad_cuda_graph_capture(shared):
+    """The knot-gradient call forks its column-direction assembly onto a helper stream and
+    joins it before returning (nurbs_api.cu): under CUDA-graph capture on a side stream the
+    replayed graph must reproduce the eager results bitwise, and the eager call on another
+    stream must not race with it (the join orders the helper stream's work)."""
+    w = wl.config4(B=32) if shared else wl.config4(B=20, knots_batched=True)
+    g = w.grad_out(5)
+    ctrl, U, V, u, v, gout = T(w.ctrl), T(w.U), T(w.V), T(w.u), T(w.v), T(g)
+    sh = nb.surface_shape(ctrl, U, u, v, w.p, w.q)
+    ws_b = nb.knots_workspace_bytes(sh)
+    ws = torch.empty(max(ws_b, 1), dtype=torch.uint8, device=ctrl.device)
+    gc, gU, gV = torch.empty_like(ctrl), torch.empty_like(U), torch.empty_like(V)
+    call = lambda st: nb.nurbs_surface_bwd_knots(sh, ctrl, U, V, u, v, None, gout, gc, gU, gV, ws, ws_b, st)  # noqa: E731
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    call(s)
+    torch.cuda.synchronize()
+    ref = (gc.clone(), gU.clone(), gV.clone())
+    for t in (gc, gU, gV):
+        t.fill_(7.0)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        call(s)
+    for _ in range(3):
+        for t in (gc, gU, gV):
+            t.fill_(-3.0)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(gc, ref[0]) and torch.equal(gU, ref[1]) and torch.equal(gV, ref[2])
