@@ -335,21 +335,25 @@ int check_ptrs(bool bwd, const void* ctrl, const void* out, const void* gout, co
 
 // ---- true knot gradients (NEXT-4): workspace = the backward's + partials + assembly buffers
 struct KnotWs {
-  size_t hU, hV, cR, sR, cC, sC, tR, tC, bytes;
+  size_t hU, hV, cR, sR, cC, sC, tR, tC, xR, bytes;
 };
 KnotWs knot_ws(const Geo& g, const Plan& pl) {
   KnotWs w{};
   const size_t B = (size_t)g.B;
   size_t o = nb::align_up(pl.ws_bytes, 256);
   auto take = [&](size_t bytes) { const size_t at = o; o = nb::align_up(o + bytes, 256); return at; };
-  w.hU = take(B * pl.NCB * g.r.ns * (g.P + 1) * 4);
+  // rows-direction units: the knot spans (span moments, grid mode 4) or the samples (mode 3)
+  const bool spans = nb::kg_span_mode(g.r.ns, g.r.n, g.P);
+  const size_t units = spans ? (size_t)(g.r.n - g.P) : (size_t)g.r.ns;
+  w.hU = take(B * pl.NCB * units * (spans ? (g.P + 1) * (g.P + 1) : (g.P + 1)) * 4);
   w.hV = take(B * pl.NRB * g.c.ns * (g.c.p + 1) * 4);
-  w.cR = take(B * g.r.ns * 2 * g.P * 4);
-  w.sR = take(B * g.r.ns * 4);
+  w.cR = take(B * units * 2 * g.P * 4);
+  w.sR = take(B * units * 4);
   w.cC = take(B * g.c.ns * 2 * g.c.p * 4);
   w.sC = take(B * g.c.ns * 4);
   w.tR = take(B * (g.r.n + g.P + 1) * 4);
   w.tC = take(B * (g.c.n + g.c.p + 1) * 4);
+  w.xR = take(spans && pl.NCB > 1 ? B * units * (g.P + 1) * (g.P + 1) * 4 : 0);  // summed span moments
   w.bytes = o;
   return w;
 }
@@ -420,18 +424,21 @@ int launch_knots(const Geo& g, const float* ctrl, const float* gout, float* gctr
   prm.hU = reinterpret_cast<float*>(w + W.hU);
   prm.hV = reinterpret_cast<float*>(w + W.hV);
   set_io_map(prm, gout, (long long)g.B * g.r.ns, g.c.ns, nb::kRPS_B);
-  cudaError_t e = nb::launch_grid(prm, 3, g.P, g.c.p, st);
+  const bool spans = nb::kg_span_mode(g.r.ns, g.r.n, g.P);
+  cudaError_t e = nb::launch_grid(prm, spans ? 4 : 3, g.P, g.c.p, st);
   if (e != cudaSuccess) return cuda_fail(e, "backward (knot gradients) kernel launch");
   if (!pl.direct && (e = nb::launch_reduce(prm, g.P, st)) != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
   const bool doR = g.P > 0 && gR;
   auto chain_v = [&](cudaStream_t sv) {
-    nb::KnotDir d{g.B, g.c.n, g.c.p, g.c.ns, g.c.knots, g.c.kstride, g.c.s, g.c.tspan, prm.hV, pl.NRB,
-                  reinterpret_cast<float*>(w + W.cC), reinterpret_cast<int*>(w + W.sC)};
+    nb::KnotDir d{g.B, g.c.n, g.c.p, g.c.ns, g.c.knots, g.c.kstride, g.c.s, g.c.tspan, prm.hV, pl.NRB, 0,
+                  reinterpret_cast<float*>(w + W.cC), reinterpret_cast<int*>(w + W.sC), nullptr};
     return nb::launch_knot_grad(d, g.c.kstride != 0, reinterpret_cast<float*>(w + W.tC), gC, sv);
   };
   auto chain_u = [&](cudaStream_t su) {
-    nb::KnotDir d{g.B, g.r.n, g.P, g.r.ns, g.r.knots, g.r.kstride, g.r.s, g.r.tspan, prm.hU, pl.NCB,
-                  reinterpret_cast<float*>(w + W.cR), reinterpret_cast<int*>(w + W.sR)};
+    // units: the n - p knot spans (span moments, mode 4) or the samples (row sums, mode 3)
+    nb::KnotDir d{g.B, g.r.n, g.P, spans ? g.r.n - g.P : g.r.ns, g.r.knots, g.r.kstride, g.r.s, g.r.tspan,
+                  prm.hU, pl.NCB, spans ? 1 : 0, reinterpret_cast<float*>(w + W.cR), reinterpret_cast<int*>(w + W.sR),
+                  reinterpret_cast<float*>(w + W.xR)};
     return nb::launch_knot_grad(d, g.r.kstride != 0, reinterpret_cast<float*>(w + W.tR), gR, su);
   };
   if (doR && gC) {  // both directions: the v chain on the helper stream, forked after the grid kernel

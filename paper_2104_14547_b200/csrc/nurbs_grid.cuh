@@ -31,7 +31,7 @@ namespace nb {
 // One row of the walk (F2, and B1 in the backward) for one column: uniform across the CTA
 // except for the column data. `nu` = basis of the row, `tw` = the T window (P+1 control rows
 // [lo, lo+P] of this column), `io` = this thread's 3 floats of the output / dL/dS row.
-template <int P, bool BWD, bool FIT, bool KG>
+template <int P, bool BWD, bool FIT, int KG>
 __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const float4 (&tw)[P + 1],
                                          float4 (&acc)[P + 1], float* io, bool valid, float fit_scale,
                                          float& lsum, float (&dots)[P + 1]) {
@@ -72,11 +72,7 @@ __device__ __forceinline__ void walk_row(const float* __restrict__ nu, const flo
     const float4 G = make_float4(gxy.x, gxy.y, gzr, -gS * rw);
 #pragma unroll
     for (int k = 0; k <= P; ++k) acc[k] = fma4v(nu[k], G, acc[k]);
-#ifdef NB_EXP_KG_NOROW
-    if constexpr (false) {
-#else
-    if constexpr (KG) {  // NEXT-4: G . T_r, the row's weight of dN_r/dU
-#endif
+    if constexpr (KG == 1) {  // NEXT-4: G . T_r, the row's weight of dN_r/dU
 #pragma unroll
       for (int k = 0; k <= P; ++k) {
         const float2 t2 = up2(ffma2(pk2(G.z, G.w), pk2(tw[k].z, tw[k].w), fmul2(pk2(G.x, G.y), pk2(tw[k].x, tw[k].y))));
@@ -209,7 +205,7 @@ __device__ __forceinline__ void b2_batch_fn(const B2Args& a, int i0, int nb) {
 // IO: how the streamed tensor (out / dL/dS / target) moves: 0 per-thread global accesses,
 // 1 TMA bulk copies (one per stage when rows are contiguous, else one per row), 2 2-D TMA
 // tensor copies (two boxes per stage; rows need not be contiguous).
-template <int P, int Q, bool BWD, int IO, bool FIT, bool KG>
+template <int P, int Q, bool BWD, int IO, bool FIT, int KG>
 #ifndef NB_MINB_F_TMAP
 #define NB_MINB_F_TMAP 6  // the tensor-map forward is shared-memory-limited to 6 CTAs: use their registers
 #endif
@@ -217,14 +213,14 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
     nurbs_grid_kernel(const __grid_constant__ Params prm) {
   constexpr bool BULK = IO >= 1;
   static_assert(!FIT || BWD, "the fitting step is a backward variant");
-  static_assert(!KG || (BWD && !FIT), "knot gradients extend the plain backward");
+  static_assert(KG == 0 || (BWD && !FIT), "knot gradients extend the plain backward");
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NP = (P + 1) <= 4 ? 4 : 8;  // floats per row-basis entry in smem
   constexpr int NQ = (Q + 1) <= 4 ? 4 : 8;  // floats per column-basis entry in smem
   constexpr int RPS = BWD ? kRPS_B : kRPS_F;      // sample rows per pipeline stage
   // stages per ring (the knot-gradient variant runs 2 so that, with its dot-product buffers,
   // four CTAs still fit an SM)
-  constexpr int NST = BWD ? (KG ? 2 : kStages_B) : kStages_F;
+  constexpr int NST = BWD ? (KG != 0 ? 2 : kStages_B) : kStages_F;
   constexpr int SROW = kCB * 3;                    // floats of one staged sample row
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -275,6 +271,11 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   int* scnt = reinterpret_cast<int*>(bars + 1 + 2 * NST);  // per slot: warps done with the stage
   // KG: [4 warps][kRowChunk][P+1], 16-byte aligned (the stage buffers behind it are read as float4)
   float* rowdot = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(scnt + NST + 2) + 15) & ~uintptr_t(15));
+  // KG == 2 (span moments): per-warp lane rows [4][32][KXS], then the per-warp
+  // span sums [4][kRMax][KNX], in the same place
+  constexpr int KNX = (P + 1) * (P + 1), KXS = KNX | 1;  // odd row stride: conflict-free columns
+  float* kxb = rowdot;
+  float* kws = kxb + (kThreads / 32) * 32 * KXS;
 
   if (tid == 0) {
     mbar_init(band_bar, 1u);
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   for (int h = 0; h <= Q; ++h) hv[h] = 0.f;
   auto flush_fast = [&](int i, float4 hrow) {
     Hring[((i - band_lo) & (kHRing - 1)) * kCB + tid] = hrow;
-    if constexpr (KG) {
+    if constexpr (KG != 0) {
       const float4* src = tb0 + (size_t)i * tstride;
 #pragma unroll
       for (int h = 0; h <= Q; ++h) {
@@ -545,8 +546,13 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
     acc[k] = f4(0.f);
   }
 
+  if constexpr (KG == 2) {  // start dot products of the first window (acc = 0) and the span sums
+    for (int x = lane; x < 32 * KXS; x += 32) kxb[warp * 32 * KXS + x] = 0.f;
+    for (int x = lane; x < kRMax * KNX; x += 32) kws[warp * kRMax * KNX + x] = 0.f;
+    __syncwarp();
+  }
   // TMA staging: columns >= cols use the unused row tail (the fit step still masks its loss)
-  const bool vio = (BULK && !FIT && !KG) ? true : valid;
+  const bool vio = (BULK && !FIT && KG == 0) ? true : valid;
   // KG: the warp sums of G . T_r per walk row -> rowdot[warp][ci][r]. Each lane parks its
   // p+1 dot products of the stage's rows in a per-warp buffer (row stride 33 floats: the
   // column reads below are bank-conflict free); at the end of the stage lane l sums one
@@ -559,22 +565,14 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   constexpr int KGS = 36, KGR = 4;  // buffer row stride, rows per buffer fill
   float* kgb = rowdot + (kThreads / 32) * kRowChunk * (P + 1) + warp * (KGR * (P + 1) * KGS);
   auto kg_row = [&](int ci, const float (&d)[P + 1]) {
-#ifdef NB_EXP_KG_NOROW
-    if constexpr (false) {
-#else
-    if constexpr (KG) {
-#endif
+    if constexpr (KG == 1) {
       const int rr = ci % KGR;
 #pragma unroll
       for (int k = 0; k <= P; ++k) kgb[(rr * (P + 1) + k) * KGS + lane] = d[k];
     }
   };
   auto kg_stage = [&](int ci0, int nr) {
-#ifdef NB_EXP_KG_NOROW
-    if constexpr (false) {
-#else
-    if constexpr (KG) {
-#endif
+    if constexpr (KG == 1) {
       __syncwarp();
       const int npair = nr * (P + 1), half = lane & 1;
       for (int base = 0; base < npair; base += 16) {  // uniform trip count (P > 3: two rounds)
@@ -598,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   // KG: rows [r0, r0 + cn) of the walk are complete in rowdot (after a barrier): warp sums in
   // warp order -> hU[s][cb][a][r] (fixed-order partial of the column block)
   auto kg_flush = [&](int r0, int cn) {
-    if constexpr (KG) {
+    if constexpr (KG == 1) {
       for (int x = tid; x < cn * (P + 1); x += kThreads) {
         const int row = x / (P + 1), k = x - row * (P + 1);
         float v = 0.f;
@@ -606,6 +604,60 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
         for (int w = 0; w < kThreads / 32; ++w) v += rowdot[(w * kRowChunk + row) * (P + 1) + k];
         prm.hU[(((size_t)s * prm.NCB + cb) * R.ns + a_lo + r0 + row) * (P + 1) + k] = v;
       }
+    }
+  };
+  // KG == 2: row-direction knot weights as span moments (NEXT-4). On a knot span
+  // the window's T rows are fixed and B1's accumulator acc[r'] gains sum_a N_r'(u_a) G_ab over
+  // the span's rows, so X[r][r'] = sum_b T_r(b) . (acc[r'] at span end - at span start) are the
+  // moments the assembly needs (the knot derivative of N_r is a combination of the span's N_r').
+  // Each lane keeps its start dot products in its kxb row; at the span end it replaces them by
+  // end - start, and the warp sums the (p+1)^2 columns over its 32 lanes (lane pairs, fixed
+  // order + one xor shuffle) into kws[warp][span - S0]. No per-row work (chosen for long spans).
+  int kg_open = 0;  // rows processed in the current window (uniform)
+  auto kdot = [](float4 a, float4 b) {
+    const float2 t = up2(ffma2(pk2(a.z, a.w), pk2(b.z, b.w), fmul2(pk2(a.x, a.y), pk2(b.x, b.y))));
+    return t.x + t.y;
+  };
+  auto kg_span_start = [&]() {  // the window just moved: start dot products (acc[p] = 0)
+    if constexpr (KG == 2) {
+      float* xr = kxb + (warp * 32 + lane) * KXS;
+#pragma unroll
+      for (int r = 0; r <= P; ++r)
+#pragma unroll
+        for (int q = 0; q < P; ++q) xr[r * (P + 1) + q] = kdot(tw[r], acc[q]);
+    }
+  };
+  auto kg_span_end = [&](int span) {  // window [lo, lo+p] = knot span lo+p is complete
+    if constexpr (KG == 2) {
+      float* xw = kxb + warp * 32 * KXS;
+      float* xr = xw + lane * KXS;
+#pragma unroll
+      for (int r = 0; r <= P; ++r) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) xr[r * (P + 1) + q] = kdot(tw[r], acc[q]) - xr[r * (P + 1) + q];
+        xr[r * (P + 1) + P] = kdot(tw[r], acc[P]);  // slot p starts every span at zero
+      }
+      __syncwarp();
+      float* dst = kws + (warp * kRMax + (span - S0)) * KNX;
+#pragma unroll
+      for (int base = 0; base < KNX; base += 16) {  // lanes (v, half): v = base + lane/2
+        const int v = base + (lane >> 1), half = lane & 1;
+        float x = 0.f;
+        if (v < KNX) {
+          float y[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) y[j] = xw[(half * 16 + j) * KXS + v];
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1)  // fixed pairwise tree
+#pragma unroll
+            for (int j = 0; j < o; ++j) y[j] += y[j + o];
+          x = y[0];
+        }
+        x += __shfl_xor_sync(0xffffffffu, x, 1);
+        if (half == 0 && v < KNX) dst[v] += x;
+      }
+      __syncwarp();
+      kg_open = 0;
     }
   };
   const float fit_scale = prm.fit_scale;
@@ -617,6 +669,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
     // unchecked mode) is evaluated with the current window — wrong values, never out of bounds
     const int target = chg ? su_s[ci] - P : lo;
     if (target > lo) {
+      if constexpr (KG == 2) {
+        if (kg_open) kg_span_end(lo + P);
+      }
 #ifndef NB_EXP_UNROLL_ADV
 #pragma unroll 1  // keep the (rare) window advance compact: unrolling it bloats the row loop
 #endif
@@ -631,7 +686,9 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
         tw[P] = Trow(lo + P);
         if constexpr (BWD) acc[P] = f4(0.f);
       } while (lo < target);
+      kg_span_start();
     }
+    if constexpr (KG == 2) kg_open = 1;
     const float* nup = Nu_s + ci * NP;
     float nu[NP];
     const float4 n0 = *reinterpret_cast<const float4*>(nup);
@@ -664,6 +721,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
         kg_row(ci0 + r, dots);
         if ((r + 1) % KGR == 0) kg_stage(ci0 + r + 1 - KGR, KGR);
       }
+      if constexpr (KG == 2) kg_open = 1;
       return;
     }
     bool fast = nr == RPS;
@@ -707,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
     const int ci0 = r0 % kRowChunk;           // kRowChunk is a multiple of RPS
     if (ci0 == 0) {                           // stage span + basis of the next kRowChunk rows
       if (r0 > 0) __syncthreads();            // previous chunk fully consumed
-      if (KG && r0 > 0) kg_flush(r0 - kRowChunk, kRowChunk);
+      if (KG == 1 && r0 > 0) kg_flush(r0 - kRowChunk, kRowChunk);
       const int cn = min(kRowChunk, nwalk - r0);
       if (row_pf) {
         const int buf = (r0 / kRowChunk) & 1;
@@ -768,9 +826,21 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
     if (++slot == NST) { slot = 0; ++use; }
   }
   if constexpr (BULK && !BWD) bulk_wait_all();  // every store this thread issued has landed
-  if constexpr (KG) {
+  if constexpr (KG == 1) {
     __syncthreads();
     if (nwalk > 0) kg_flush((nstage - 1) * RPS / kRowChunk * kRowChunk, nwalk - (nstage - 1) * RPS / kRowChunk * kRowChunk);
+  }
+  if constexpr (KG == 2) {  // the last span's moments, then this tile's sums in warp order -> hU
+    if (kg_open) kg_span_end(lo + P);
+    __syncthreads();
+    const int nsp = R.n - P;
+    for (int x = tid; x < (S1 - S0) * KNX; x += kThreads) {
+      const int sr = x / KNX, v = x - sr * KNX;
+      float acc_x = 0.f;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) acc_x += kws[(w * kRMax + sr) * KNX + v];
+      prm.hU[(((size_t)s * prm.NCB + cb) * nsp + (S0 - P + sr)) * KNX + v] = acc_x;
+    }
   }
 
   if constexpr (BWD) {
@@ -789,13 +859,13 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
       __syncthreads();
       if (tid == 0) prm.loss_parts[blockIdx.x] = (lw[0] + lw[1]) + (lw[2] + lw[3]);
     }
-    if constexpr (KG) {  // this tile's partial of hV[s][rb][b][h]
+    if constexpr (KG != 0) {  // this tile's partial of hV[s][rb][b][h]
       if (valid)
 #pragma unroll
         for (int h = 0; h <= Q; ++h) prm.hV[(((size_t)s * prm.NRB + rb) * C.ns + B0 + tid) * (Q + 1) + h] = hv[h];
     }
     if (!prm.direct && rb == 0 && tid == 0) prm.colband[(size_t)s * prm.NCB + cb] = make_int2(sfirst - Q, sfirst + nspan - 1);
-    if (prm.direct && !KG) {  // knot gradients are zero by definition
+    if (prm.direct && KG == 0) {  // knot gradients are zero by definition
       if (prm.gR && s < prm.gR_items)
         for (int x = tid; x < prm.gR_per; x += kThreads) prm.gR[(size_t)s * prm.gR_per + x] = 0.f;
       if (prm.gC && s < prm.gC_items)
@@ -804,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? kMinBlocks_B : (IO == 2 ? NB_M
   }
 }
 
-template <int P, int Q, bool BWD, int IO, bool FIT, bool KG = false>
+template <int P, int Q, bool BWD, int IO, bool FIT, int KG = 0>
 static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
   const size_t smem = grid_smem_bytes(BWD, P, Q, prm.T_rows, prm.CBW, KG, IO == 2);
   // the dynamic shared-memory opt-in is per device (a benign race: setting it twice is harmless)
@@ -824,10 +894,12 @@ static cudaError_t launch_one(const Params& prm, cudaStream_t st) {
 }
 
 // mode: 0 forward, 1 backward, 2 fused fitting step (backward with dL/dS from a target),
-// 3 backward with the knot-gradient partials (NEXT-4)
+// 3 backward with the knot-gradient partials (NEXT-4; per-row weights), 4 the same with
+// span moments for the rows direction
 template <int P, int Q, int IO>
 static cudaError_t launch_pq_io(const Params& prm, int mode, cudaStream_t st) {
-  if (mode == 3) return launch_one<P, Q, true, IO, false, true>(prm, st);
+  if (mode == 4) return launch_one<P, Q, true, IO, false, 2>(prm, st);
+  if (mode == 3) return launch_one<P, Q, true, IO, false, 1>(prm, st);
   if (mode == 2) return launch_one<P, Q, true, IO, true>(prm, st);
   if (mode == 1) return launch_one<P, Q, true, IO, false>(prm, st);
   return launch_one<P, Q, false, IO, false>(prm, st);

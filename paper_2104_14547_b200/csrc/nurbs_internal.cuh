@@ -97,7 +97,8 @@ struct Params {
   float lr;
   int n_parts;
   // true knot gradients (NEXT-4, mode 3)
-  float* hU;                // [B][NCB][r.ns][P+1]: sum over the block's columns of G . T_r
+  float* hU;                // mode 3: [B][NCB][r.ns][P+1] row sums of G . T_r; mode 4:
+                            // [B][NCB][r.n-P][(P+1)^2] span moments X[r][r'] (nurbs_grid.cuh)
   float* hV;                // [B][NRB][c.ns][q+1]: sum over the band rows of Q[i][sv-q+h] . H[i][b]
   // 2-D TMA descriptor of the streamed tensor (out in the forward, dL/dS or the target in the
   // backward / fitting step) viewed as [B*n_u rows][n_v*3 floats], box = RPS rows x 192 floats
@@ -208,6 +209,15 @@ inline Plan make_plan(int B, int n_r, int P, int ns_r, int n_c, int ns_c, bool f
   return pl;
 }
 
+// Knot-gradient mode of a surface shape (NEXT-4): span moments (grid mode 4) when the rows
+// direction has at least kKgSpanRows sample rows per knot span on average (the per-span work
+// then beats per-row dot products: config 5's 32 rows per span 0.335 -> 0.27 ms; config 4's
+// 10 rows per span keep per-row weights, measured 0.368 vs 0.385 ms), else per-row (mode 3).
+constexpr int kKgSpanRows = 16;
+inline bool kg_span_mode(int ns_r, int n_r, int P) {
+  return P > 0 && (long long)ns_r >= (long long)kKgSpanRows * (n_r - P);
+}
+
 // Launchers (nurbs_kernels.cu). Return cudaError_t of the launch.
 cudaError_t launch_grid(const Params& prm, int mode, int P, int q, cudaStream_t st);  // mode 0 fwd, 1 bwd, 2 fit
 cudaError_t launch_reduce(const Params& prm, int P, cudaStream_t st);
@@ -226,7 +236,7 @@ cudaError_t launch_validate(int B, const Dir& r, const Dir& c, int check_rows,
 bool bwd_tc_supported(const Params& prm, int P, int q);
 cudaError_t launch_bwd_tc(const Params& prm, int P, int q, cudaStream_t st);
 cudaError_t launch_sum_partials(const float* parts, int np, long long n, float* out, cudaStream_t st);
-size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg = false, bool tmap = false);
+size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, int kg = 0, bool tmap = false);
 
 }  // namespace nb
 

@@ -168,18 +168,22 @@ __global__ void nurbs_validate_kernel(int B, Dir R, Dir C, int check_rows, const
 }
 
 // ------------------------------------------------------------------------ launchers
-size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, bool kg, bool tmap) {
+size_t grid_smem_bytes(bool bwd, int P, int q, int T_rows, int CBW, int kg, bool tmap) {
   const int NP = (P + 1) <= 4 ? 4 : 8;
   const int NQ = (q + 1) <= 4 ? 4 : 8;
-  const int rps = bwd ? kRPS_B : kRPS_F, nst = bwd ? (kg ? 2 : kStages_B) : kStages_F;
+  const int rps = bwd ? kRPS_B : kRPS_F, nst = bwd ? (kg != 0 ? 2 : kStages_B) : kStages_F;
   const int nrt = tmap && P > 0 && !bwd ? 2 : 1;  // row tables double-buffered (tensor-map forward)
   size_t b = (((size_t)T_rows * CBW * 16 + 127) & ~(size_t)127) + (size_t)nst * rps * kCB * 3 * 4 + nrt * kRowChunk * 4 +
              (size_t)nrt * kRowChunk * NP * 4;
   if (bwd) b += (size_t)kHRing * kCB * 16 + kCB * 4 + (size_t)kCB * NQ * 4 + (kCB + 4) * 4;
   b += 4 * 4;                                  // misc
   b = (b + 7) / 8 * 8 + (1 + 2 * nst) * 8 + nst * 4;  // mbarriers + stage counters
-  if (kg)  // rowdot + the per-warp stage buffers of the row dot products (NEXT-4)
+  if (kg == 1)  // rowdot + the per-warp stage buffers of the row dot products (NEXT-4)
     b += 16 + (size_t)(kThreads / 32) * kRowChunk * (P + 1) * 4 + (size_t)(kThreads / 32) * 4 * (P + 1) * 36 * 4;
+  if (kg == 2) {  // span moments (NEXT-4): per-warp lane rows [4][32][KXS] + span sums [4][kRMax][KNX]
+    const int knx = (P + 1) * (P + 1), kxs = knx | 1;
+    b += 16 + (size_t)(kThreads / 32) * 32 * kxs * 4 + (size_t)(kThreads / 32) * kRMax * knx * 4;
+  }
   return b;
 }
 

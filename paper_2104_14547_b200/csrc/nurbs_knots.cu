@@ -2,9 +2,15 @@
 // gradients as zero (§3.2.2); this extension differentiates the basis with respect to
 // the knots. For one direction (rows = u shown; columns = v alike):
 //   dL/dU_k = sum_a sum_r dN_r(u_a)/dU_k * h_r(a),   h_r(a) = sum_b G_ab . T_r(a, b)
-// where G = (g/W, -(g.S)/W) is the backward's homogeneous upstream and T_r the F1 row
-// (the grid kernel's mode 3 writes h per (surface, column block, row), nurbs_grid.cuh); for
-// the v direction h_h(b) = sum_i Q[i][sv(b)-q+h] . H[i][b] with H = N_u^T G (B1's output).
+// where G = (g/W, -(g.S)/W) is the backward's homogeneous upstream and T_r the F1 row; for
+// the v direction h_h(b) = sum_i Q[i][sv(b)-q+h] . H[i][b] with H = N_u^T G (B1's output),
+// written per (surface, row block, column). For the u direction the grid kernel writes span
+// moments instead (nurbs_knot_spans_kernel below): on knot span s the derivative of each
+// non-zero basis function is a degree-p polynomial, i.e. a combination of the span's p+1
+// basis functions, dN_r/dU_k = sum_r' C[r][k][r'] N_r', so
+//   sum_{a in s} dN_r(u_a)/dU_k h_r(a) = sum_r' C[r][k][r'] X[r][r'],
+//   X[r][r'] = sum_{a in s} N_r'(u_a) h_r(a) = sum_b T_r(b) . (sum_{a in s} N_r'(u_a) G_ab).
+// C comes from a (p+1) x (p+1) collocation solve on the span (fp64).
 // dN_r/dU_k is forward-mode differentiation of the A2.2 triangle along each of the
 // 2p knots U[s-p+1 .. s+p] it reads. Every sum runs in a fixed order (deterministic).
 // Citations: P:n = reference/PAPER.md line n; R<k> = DESIGN.md §3 reading k.
@@ -126,6 +132,130 @@ __global__ void nurbs_knot_rows_kernel(KnotDir d) {
   d.span[idx] = sp;
 }
 
+// out[s][e] = sum over the nparts partials part[s][c][e] (ascending c): the span moments of
+// the column blocks / row blocks summed once before the per-(span, knot) threads read them.
+__global__ void nurbs_knot_partsum_kernel(const float* __restrict__ part, long long B, int nparts, int E,
+                                          float* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * E) return;
+  const long long s = idx / E;
+  const int e = (int)(idx - s * E);
+  const float* src = part + (size_t)s * nparts * E + e;
+  float acc = 0.f;
+  int c = 0;
+  for (; c + 4 <= nparts; c += 4) {  // four loads in flight, added in part order
+    const float a0 = __ldg(src + (size_t)c * E), a1 = __ldg(src + (size_t)(c + 1) * E);
+    const float a2 = __ldg(src + (size_t)(c + 2) * E), a3 = __ldg(src + (size_t)(c + 3) * E);
+    acc += a0; acc += a1; acc += a2; acc += a3;
+  }
+  for (; c < nparts; ++c) acc += __ldg(src + (size_t)c * E);
+  out[idx] = acc;
+}
+
+// Rows direction from span moments (d.spans == 1, unit k = knot span s = p + k): one thread per
+// (surface, span, knot t). X[r][r'] = sum over the nparts partials (ascending). With p+1
+// Chebyshev points u_m of the span, A[m][r'] = N_r'(u_m) and Z A = X (Z: r x m, fp64 LU with
+// partial pivoting of A^T), the span's contribution to knot U[s-p+1+t] is
+//   sum_{r,r'} C[r][t][r'] X[r][r'] = sum_m sum_r dN_r(u_m)/dU_t Z[r][m]
+// (C[r][t][.] = A^-1 applied to dN_r/dU_t at the points), i.e. p+1 dual-number A2.2 passes.
+template <int P>
+__global__ void nurbs_knot_spans_kernel(KnotDir d) {
+  constexpr int NX = (P + 1) * (P + 1);
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)d.B * d.ns * (2 * P)) return;
+  const long long sk = idx / (2 * P);
+  const int t = (int)(idx - sk * (2 * P));
+  const int sf = (int)(sk / d.ns), k = (int)(sk - (long long)sf * d.ns);
+  const int sp = P + k;
+  if (t == 0) d.span[sk] = sp;
+  const float* Uk = d.knots + (long long)sf * d.kstride;
+  const float ua = __ldg(Uk + sp), ub = __ldg(Uk + sp + 1);
+  float res = 0.f;
+  if (ub > ua) {  // empty spans hold no samples: no contribution
+    float X[NX];
+#pragma unroll
+    for (int v = 0; v < NX; ++v) X[v] = 0.f;
+    const float* src = d.part + ((size_t)sf * d.nparts * d.ns + k) * NX;
+    for (int c = 0; c < d.nparts; ++c)
+#pragma unroll
+      for (int v = 0; v < NX; ++v) X[v] += __ldg(src + (size_t)c * d.ns * NX + v);
+    float um[P + 1];
+    double At[P + 1][P + 1];  // At[r'][m] = N_r'(u_m)
+#pragma unroll
+    for (int m = 0; m <= P; ++m) {
+      const float c = 0.5f * (1.f - cospif((2.f * m + 1.f) / (2.f * (P + 1))));
+      um[m] = fmaf(ub - ua, c, ua);
+      float N[P + 1];
+      d_basis<P>(Uk, sp, um[m], P, N);
+#pragma unroll
+      for (int r = 0; r <= P; ++r) At[r][m] = (double)N[r];
+    }
+    // Z A = X  <=>  A^T Z^T = X^T: LU of At (partial pivoting), then P+1 right-hand sides
+    int piv[P + 1];
+#pragma unroll
+    for (int i = 0; i <= P; ++i) piv[i] = i;
+#pragma unroll
+    for (int c = 0; c <= P; ++c) {  // (fully unrolled: At stays in registers; swaps by selects)
+      int pr = c;
+      double best = fabs(At[c][c]);
+#pragma unroll
+      for (int i = c + 1; i <= P; ++i)
+        if (fabs(At[i][c]) > best) { best = fabs(At[i][c]); pr = i; }
+#pragma unroll
+      for (int i = c + 1; i <= P; ++i) {
+        if (i == pr) {
+#pragma unroll
+          for (int j = 0; j <= P; ++j) { const double tmp = At[c][j]; At[c][j] = At[i][j]; At[i][j] = tmp; }
+          const int ti = piv[c]; piv[c] = piv[i]; piv[i] = ti;
+        }
+      }
+      const double rinv = 1.0 / At[c][c];
+#pragma unroll
+      for (int i = c + 1; i <= P; ++i) {
+        const double f = At[i][c] * rinv;
+        At[i][c] = f;
+#pragma unroll
+        for (int j = c + 1; j <= P; ++j) At[i][j] -= f * At[c][j];
+      }
+    }
+    float kn[2 * P];
+#pragma unroll
+    for (int q = 0; q < 2 * P; ++q) kn[q] = __ldg(Uk + sp - P + 1 + q);
+    float Z[P + 1][P + 1];  // Z[r][m]
+#pragma unroll
+    for (int r = 0; r <= P; ++r) {  // solve At z = (X[r][0..P]) with the row permutation piv
+      double y[P + 1];
+#pragma unroll
+      for (int i = 0; i <= P; ++i) {
+        double xv = 0.0;
+#pragma unroll
+        for (int q = 0; q <= P; ++q)
+          if (piv[i] == q) xv = (double)X[r * (P + 1) + q];
+#pragma unroll
+        for (int j = 0; j < i; ++j) xv -= At[i][j] * y[j];
+        y[i] = xv;
+      }
+#pragma unroll
+      for (int i = P; i >= 0; --i) {
+        double a = y[i];
+#pragma unroll
+        for (int j = i + 1; j <= P; ++j) a -= At[i][j] * y[j];
+        y[i] = a / At[i][i];
+      }
+#pragma unroll
+      for (int m = 0; m <= P; ++m) Z[r][m] = (float)y[m];
+    }
+#pragma unroll
+    for (int m = 0; m <= P; ++m) {
+      float h[P + 1];
+#pragma unroll
+      for (int r = 0; r <= P; ++r) h[r] = Z[r][m];
+      res += d_basis_dknot_one<P>(kn, um[m], h, t);
+    }
+  }
+  d.contrib[(size_t)sk * (2 * P) + t] = res;
+}
+
 // Per (surface, knot k): sum over the samples whose span window holds k (spans are
 // non-decreasing in the sorted samples, so the window is a contiguous range). One warp per
 // (surface, knot): lane l sums samples lo+l, lo+l+32, ... in ascending order, then a fixed
@@ -217,6 +347,18 @@ __global__ void __launch_bounds__(256) nurbs_knot_htree_kernel(const float* __re
 
 static cudaError_t launch_rows(const KnotDir& d, cudaStream_t st) {
   const long long rows = (long long)d.B * d.ns;
+  if (d.spans) {
+    const unsigned nbt = (unsigned)((rows * 2 * d.p + 127) / 128);
+    switch (d.p) {
+      case 1: nurbs_knot_spans_kernel<1><<<nbt, 128, 0, st>>>(d); break;
+      case 2: nurbs_knot_spans_kernel<2><<<nbt, 128, 0, st>>>(d); break;
+      case 3: nurbs_knot_spans_kernel<3><<<nbt, 128, 0, st>>>(d); break;
+      case 4: nurbs_knot_spans_kernel<4><<<nbt, 128, 0, st>>>(d); break;
+      case 5: nurbs_knot_spans_kernel<5><<<nbt, 128, 0, st>>>(d); break;
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+  }
   if (d.nparts == 1) {
     const unsigned nbt = (unsigned)((rows * 2 * d.p + 127) / 128);
     switch (d.p) {
@@ -246,7 +388,7 @@ cudaError_t launch_knot_grad(const KnotDir& d, bool batched, float* tmp, float* 
   if (!batched && d.B >= 16 && d.ns > 0) {
     // workspace (d.contrib holds B*ns*2p floats): [G][ns][p+1] group sums, [ns][p+1] batch
     // sum, then the one surface's [ns][2p] contributions
-    const int E = d.ns * (d.p + 1);
+    const int E = d.ns * (d.spans ? (d.p + 1) * (d.p + 1) : d.p + 1);
     const long long cap = (long long)d.B * d.ns * 2 * d.p;
     long long G = (cap - (long long)d.ns * 2 * d.p - E) / E;
     G = G > 256 ? 256 : G;
@@ -274,7 +416,17 @@ cudaError_t launch_knot_grad(const KnotDir& d, bool batched, float* tmp, float* 
   }
   const int nk = d.n + d.p + 1;
   if (d.ns > 0) {
-    cudaError_t e = launch_rows(d, st);
+    KnotDir dr = d;
+    if (d.spans && d.nparts > 1) {  // sum the partials once (d.xsum: [B][ns][(p+1)^2])
+      const int E = d.ns * (d.p + 1) * (d.p + 1);
+      const long long th = (long long)d.B * E;
+      nurbs_knot_partsum_kernel<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(d.part, d.B, d.nparts, E, d.xsum);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      dr.part = d.xsum;
+      dr.nparts = 1;
+    }
+    cudaError_t e = launch_rows(dr, st);
     if (e != cudaSuccess) return e;
   }
   float* dst = batched ? out : tmp;

@@ -13,10 +13,14 @@ struct KnotDir {             // one parametric direction
   long long kstride;         // 0 = shared
   const float* samples;      // [ns], non-decreasing
   const int* tspan;          // optional span table
-  const float* part;         // [B][nparts][ns][p+1] partial h
+  const float* part;         // [B][nparts][ns][hlen] partial weights
   int nparts;
+  int spans;                 // 0: units are samples, part = h [p+1] per sample;
+                             // 1: units are the n-p knot spans (ns = n-p), part = span moments
+                             //    X [(p+1)^2] per span (grid kernel mode 3, rows direction)
   float* contrib;            // [B][ns][2p] workspace
   int* span;                 // [B][ns] workspace
+  float* xsum;               // spans with nparts > 1: [B][ns][(p+1)^2] workspace (else unused)
 };
 
 // dL/d(knots) of one direction into out ([B][nk] if batched, else [nk] via tmp [B][nk]).

@@ -19,6 +19,8 @@ VARIANTS = {
     "nob2": ["-DNB_EXP_NO_B2"],
     "kgnorow": ["-DNB_EXP_KG_NOROW"],
     "kasm": [],
+    "kspan": [],
+    "kmix": [],
     "ptspk": [],
     "ptsnopk": ["-DNB_PTS_NO_PACKED_BASIS"],
     "ptsg4": ["-DNB_KGRP=4"],

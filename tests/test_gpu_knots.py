@@ -72,6 +72,26 @@ def test_knot_grad_shared_knots_batch_first_sum(B, p, q, n_v):
     check(w)
 
 
+@pytest.mark.parametrize("p,q", [(1, 1), (3, 3), (5, 5), (2, 4)])
+@pytest.mark.parametrize("B,batched", [(3, False), (3, True), (20, False)])
+def test_knot_grad_span_moments(p, q, B, batched):
+    """Shapes with >= 16 sample rows per knot span take the span-moment path (grid mode 4 +
+    the per-span collocation assembly, nurbs_knots.cu): 5 spans x 20 rows, against the oracle
+    (shared knots with B >= 16 sum the span moments over the batch first)."""
+    w = wl.surfaces(f"ks{p}{q}", B, p + 5, q + 6, p, q, 100, 45, seed=p + 3 * q + B, knots_batched=batched)
+    check(w)
+
+
+def test_knot_grad_span_moments_tiled():
+    """Span moments with several row blocks and column blocks (partials summed per span
+    before the assembly) and with the precomputed tables."""
+    w = wl.surfaces("kst", 1, 40, 10, 3, 3, 629, 300, seed=21)   # 37 spans x 17 rows, NCB = 3
+    check(w)
+    check(w, tables=True)
+    w2 = wl.surfaces("kst5", 2, 64, 12, 3, 3, 1024, 256, seed=22)  # 61 spans x 16.8 rows
+    check(w2)
+
+
 def test_knot_grad_tiled_and_tables():
     """Several row and column blocks (the reduce path, several partials per sample)."""
     w = wl.surfaces("tiled", 1, 12, 10, 3, 3, 50, 260, seed=8)   # NRB = 9 row blocks, NCB = 3
