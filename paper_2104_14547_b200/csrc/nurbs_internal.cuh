@@ -213,7 +213,10 @@ inline Plan make_plan(int B, int n_r, int P, int ns_r, int n_c, int ns_c, bool f
 // direction has at least kKgSpanRows sample rows per knot span on average (the per-span work
 // then beats per-row dot products: config 5's 32 rows per span 0.335 -> 0.27 ms; config 4's
 // 10 rows per span keep per-row weights, measured 0.368 vs 0.385 ms), else per-row (mode 3).
-constexpr int kKgSpanRows = 16;
+#ifndef NB_KG_SPAN_ROWS
+#define NB_KG_SPAN_ROWS 16
+#endif
+constexpr int kKgSpanRows = NB_KG_SPAN_ROWS;
 inline bool kg_span_mode(int ns_r, int n_r, int P) {
   return P > 0 && (long long)ns_r >= (long long)kKgSpanRows * (n_r - P);
 }

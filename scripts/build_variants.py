@@ -21,6 +21,7 @@ VARIANTS = {
     "kasm": [],
     "kspan": [],
     "kmix": [],
+    "kspan8": ["-DNB_KG_SPAN_ROWS=8"],
     "ptspk": [],
     "ptsnopk": ["-DNB_PTS_NO_PACKED_BASIS"],
     "ptsg4": ["-DNB_KGRP=4"],
