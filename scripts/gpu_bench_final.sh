@@ -25,6 +25,6 @@ NB_BENCH_SHARE_GPU=1 run --config 5 --gpus 2 --steps 5 --warmup 3 --no-cpu-basel
 if [ -z "$SKIP_NCU" ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_cfg4.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
   ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_cfg5.csv python bench.py --config 5 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:nurbs_grid_kernel -s 6 -c 2 -f -o $O/prof_cfg4 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:nurbs_grid_kernel -s 6 -c 2 -f -o $O/prof_cfg5 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+  [ -n "$FULL" ] && ncu --set full --clock-control none --import-source on -k regex:nurbs_grid_kernel -s 6 -c 2 -f -o $O/prof_cfg4 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+  [ -n "$FULL" ] && ncu --set full --clock-control none --import-source on -k regex:nurbs_grid_kernel -s 6 -c 2 -f -o $O/prof_cfg5 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 fi
