@@ -1062,8 +1062,36 @@ def run_grid(args, rank, world, local):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = te.item() / E
+        # the PCIe ceiling of this step: the same byte volumes copied both ways at once (no
+        # kernels), pinned host buffers on two streams (scripts/pcie_probe.py measures it alone)
+        s_a, s_b = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+        def copies():
+            s_a.wait_stream(stream)
+            s_b.wait_stream(stream)
+            with torch.cuda.stream(s_a):
+                gout.copy_(h_gout, non_blocking=True)
+                ctrl.copy_(h_ctrl, non_blocking=True)
+            with torch.cuda.stream(s_b):
+                h_out.copy_(out, non_blocking=True)
+                h_grad.copy_(ctrl, non_blocking=True)
+            stream.wait_stream(s_a)
+            stream.wait_stream(s_b)
+
+        copies()
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(3):
+            copies()
+        c1.record(stream)
+        torch.cuda.synchronize()
+        ceil_ms = c0.elapsed_time(c1) / 3
         e2e = {"value": all_points / (e2e_ms * 1e-3), "unit": "points/s", "h2d_bytes_per_step": pipe.h2d_bytes(B),
                "d2h_bytes_per_step": pipe.d2h_bytes(B), "ms_per_step": e2e_ms,
+               "pcie_ceiling": {"ms_per_step": ceil_ms, "value": all_points / (ceil_ms * 1e-3),
+                                "frac": ceil_ms / e2e_ms,
+                                "note": "the step's h2d and d2h bytes copied both ways at once, no kernels"},
                "note": f"pinned host ctrl+grad_out -> device, fwd+bwd via the C ABI, out+grad_ctrl -> host; "
                        f"HostBatchPipeline, chunks of {chunk} surfaces on h2d/compute/d2h streams (per rank)"}
     elif not args.no_e2e:
