@@ -166,6 +166,10 @@ size_t nurbs_surface_fit_workspace_bytes(const nurbs_shape* shape);
  * one per surface. u / v must be non-decreasing (the grid); U, V, u, v may not be NULL even
  * with tables. Workspace: nurbs_*_bwd_knots_workspace_bytes(shape) bytes (never 0).
  * Deterministic (fixed-order sums). Curves: grad_U receives the curve's knot gradient.
+ * Asynchronous on `stream`: the column-direction assembly runs on an internal per-device
+ * helper stream forked from and joined back into `stream` with events (CUDA-graph capturable).
+ * When the rows direction has >= 16 samples per knot span the row weights are formed as span
+ * moments; the result is the same derivative up to rounding.
  * --------------------------------------------------------------------------------------- */
 int    nurbs_surface_bwd_knots(const nurbs_shape* shape, const float* ctrl,
                                const float* U, const float* V, const float* u, const float* v,
