@@ -172,3 +172,22 @@ def test_knot_grad_cuda_graph_capture(shared):
         graph.replay()
         torch.cuda.synchronize()
         assert torch.equal(gc, ref[0]) and torch.equal(gU, ref[1]) and torch.equal(gV, ref[2])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_knot_grad_span_moments_fuzz(seed):
+    """Span-moment mode on random shapes with non-uniform shared knots (one interior knot
+    doubled where there is room: an empty span whose moments are zero), degrees 1..5, small and
+    batch-first (B >= 16) batches, against the oracle at the stated tolerance."""
+    rng = np.random.default_rng(900 + seed)
+    p, q = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+    n, m = p + int(rng.integers(2, 7)), q + int(rng.integers(2, 7))
+    n_u, n_v = 16 * (n - p) + int(rng.integers(0, 41)), int(rng.integers(5, 140))
+    B = int(rng.choice([2, 17]))
+    w = wl.surfaces(f"ksf{seed}", B, n, m, p, q, n_u, n_v, seed=seed)
+    U = wl.random_clamped_knots(rng, n, p)
+    if n - p - 1 >= 2:
+        k = p + 1 + int(rng.integers(0, n - p - 2))
+        U[k + 1] = U[k]
+    w = wl.Surfaces(w.name, p, q, w.ctrl, U.astype(np.float32), w.V, w.u, w.v, False)
+    check(w)
