@@ -21,6 +21,9 @@ VARIANTS = {
     "kasm": [],
     "kspan": [],
     "kmix": [],
+    "l2pf1": ["-DNB_EXP_L2PF=1"],
+    "l2pf2": ["-DNB_EXP_L2PF=2"],
+    "base2": [],
     "kspan8": ["-DNB_KG_SPAN_ROWS=8"],
     "ptspk": [],
     "ptsnopk": ["-DNB_PTS_NO_PACKED_BASIS"],
