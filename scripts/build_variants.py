@@ -21,6 +21,9 @@ VARIANTS = {
     "kasm": [],
     "kspan": [],
     "kmix": [],
+    "kc8": ["-DNB_KG_SPAN_ROWS=8"],
+    "knc8": ["-DNB_KG_SPAN_ROWS=8", "-DNB_NO_KG_CARRY"],
+    "kc16": [],
     "l2pf1": ["-DNB_EXP_L2PF=1"],
     "l2pf2": ["-DNB_EXP_L2PF=2"],
     "base2": [],
