@@ -353,7 +353,8 @@ KnotWs knot_ws(const Geo& g, const Plan& pl) {
   w.sC = take(B * g.c.ns * 4);
   w.tR = take(B * (g.r.n + g.P + 1) * 4);
   w.tC = take(B * (g.c.n + g.c.p + 1) * 4);
-  w.xR = take(spans && pl.NCB > 1 ? B * units * (g.P + 1) * (g.P + 1) * 4 : 0);  // summed span moments
+  w.xR = take(spans && pl.NCB > nb::kKnotPartGroups ? B * nb::kKnotPartGroups * units * (g.P + 1) * (g.P + 1) * 4
+                                                     : 0);  // group sums of the span moments
   w.bytes = o;
   return w;
 }

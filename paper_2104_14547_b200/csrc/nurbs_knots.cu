@@ -132,23 +132,27 @@ __global__ void nurbs_knot_rows_kernel(KnotDir d) {
   d.span[idx] = sp;
 }
 
-// out[s][e] = sum over the nparts partials part[s][c][e] (ascending c): the span moments of
-// the column blocks / row blocks summed once before the per-(span, knot) threads read them.
-__global__ void nurbs_knot_partsum_kernel(const float* __restrict__ part, long long B, int nparts, int E,
+// out[s][g][e] = sum over the partials c of group g (parts [g*np/G, (g+1)*np/G), ascending)
+// of part[s][c][e]: the span moments of the column blocks summed in G fixed groups, in
+// parallel, before the per-(span, knot) threads add the G group sums (ascending g).
+__global__ void nurbs_knot_partsum_kernel(const float* __restrict__ part, long long B, int nparts, int E, int G,
                                           float* __restrict__ out) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= B * E) return;
-  const long long s = idx / E;
-  const int e = (int)(idx - s * E);
+  if (idx >= B * G * E) return;
+  const long long sg = idx / E;
+  const int e = (int)(idx - sg * E);
+  const long long s = sg / G;
+  const int g = (int)(sg - s * G);
+  const int c0 = (int)((long long)nparts * g / G), c1 = (int)((long long)nparts * (g + 1) / G);
   const float* src = part + (size_t)s * nparts * E + e;
   float acc = 0.f;
-  int c = 0;
-  for (; c + 4 <= nparts; c += 4) {  // four loads in flight, added in part order
+  int c = c0;
+  for (; c + 4 <= c1; c += 4) {  // four loads in flight, added in part order
     const float a0 = __ldg(src + (size_t)c * E), a1 = __ldg(src + (size_t)(c + 1) * E);
     const float a2 = __ldg(src + (size_t)(c + 2) * E), a3 = __ldg(src + (size_t)(c + 3) * E);
     acc += a0; acc += a1; acc += a2; acc += a3;
   }
-  for (; c < nparts; ++c) acc += __ldg(src + (size_t)c * E);
+  for (; c < c1; ++c) acc += __ldg(src + (size_t)c * E);
   out[idx] = acc;
 }
 
@@ -417,14 +421,15 @@ cudaError_t launch_knot_grad(const KnotDir& d, bool batched, float* tmp, float* 
   const int nk = d.n + d.p + 1;
   if (d.ns > 0) {
     KnotDir dr = d;
-    if (d.spans && d.nparts > 1) {  // sum the partials once (d.xsum: [B][ns][(p+1)^2])
+    if (d.spans && d.nparts > kKnotPartGroups) {  // partials -> kKnotPartGroups group sums (d.xsum)
       const int E = d.ns * (d.p + 1) * (d.p + 1);
-      const long long th = (long long)d.B * E;
-      nurbs_knot_partsum_kernel<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(d.part, d.B, d.nparts, E, d.xsum);
+      const long long th = (long long)d.B * kKnotPartGroups * E;
+      nurbs_knot_partsum_kernel<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(d.part, d.B, d.nparts, E,
+                                                                              kKnotPartGroups, d.xsum);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       dr.part = d.xsum;
-      dr.nparts = 1;
+      dr.nparts = kKnotPartGroups;
     }
     cudaError_t e = launch_rows(dr, st);
     if (e != cudaSuccess) return e;

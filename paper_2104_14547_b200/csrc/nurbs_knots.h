@@ -20,8 +20,12 @@ struct KnotDir {             // one parametric direction
                              //    X [(p+1)^2] per span (grid kernel mode 3, rows direction)
   float* contrib;            // [B][ns][2p] workspace
   int* span;                 // [B][ns] workspace
-  float* xsum;               // spans with nparts > 1: [B][ns][(p+1)^2] workspace (else unused)
+  float* xsum;               // spans with nparts > kKnotPartGroups: [B][groups][ns][(p+1)^2] workspace
 };
+
+// Span-moment partials are summed in this many fixed groups first (nurbs_knot_partsum_kernel);
+// the workspace's xsum holds [B][kKnotPartGroups][ns][(p+1)^2].
+constexpr int kKnotPartGroups = 8;
 
 // dL/d(knots) of one direction into out ([B][nk] if batched, else [nk] via tmp [B][nk]).
 cudaError_t launch_knot_grad(const KnotDir& d, bool batched, float* tmp, float* out, cudaStream_t st);
