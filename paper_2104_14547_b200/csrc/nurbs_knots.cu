@@ -272,11 +272,26 @@ __global__ void nurbs_knot_gather_kernel(KnotDir d, float* out /* [B][nk] */) {
   const int s = (int)(idx / nk), k = (int)(idx - (long long)s * nk);
   const int p = d.p;
   const int* sp = d.span + (size_t)s * d.ns;
-  // rows with span in [k - p, k + p - 1] contribute to knot k (t = k - (span - p + 1))
+  // rows with span in [k - p, k + p - 1] contribute to knot k (t = k - (span - p + 1));
+  // lo = the first of them. Units that are the knot spans themselves (span p + a at a) index
+  // it directly; samples: a warp-wide search, 32 probes per round (one load latency per
+  // 32x narrowing instead of one per halving)
+  const int key = k - p;
   int lo = 0, hi = d.ns;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (sp[mid] < k - p) lo = mid + 1; else hi = mid;
+  if (d.spans) {
+    lo = hi = min(max(key - p, 0), d.ns);
+  }
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) / 32;
+    const bool lt = sp[min(lo + step * lane, hi - 1)] < key;  // non-decreasing probes: a prefix
+    const int c = __popc(__ballot_sync(0xffffffffu, lt));
+    const int nlo = c == 0 ? lo : min(hi, lo + step * (c - 1) + 1);
+    hi = c == 32 ? hi : min(hi, lo + step * c);
+    lo = nlo;
+  }
+  if (hi > lo) {
+    const bool lt = lo + lane < hi && sp[lo + lane] < key;
+    lo += __popc(__ballot_sync(0xffffffffu, lt));
   }
   float acc = 0.f;
   for (int a = lo + lane; a < d.ns; a += 32) {
